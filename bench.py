@@ -1,0 +1,360 @@
+#!/usr/bin/env python
+"""Benchmark: MHD cell-updates/s of the PPMLR time step on B200.
+
+One "step" is one Harness::advance (CFL dt, the three directional PPMLR
+sweeps in XYZ/ZYX order, dipole sources, frozen core) over the whole
+synthetic grid.  Default workload: C4 of BASELINE.json, the
+weak-scaling blast wave, 512^3 cells per GPU (x-slab per rank).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config blast512]
+                  [--precision strict|fast] [--impl ours|reference]
+
+For N>1 launch one rank per GPU with torch.distributed.run (NCCL); the
+halo exchange and the dt min-reduction go through torch.distributed.
+
+Prints ONE JSON line (rank 0).  value = whole-job cell-updates/s timed with
+CUDA events on the block's stream (max over ranks); e2e = the same metric
+through the public API with host buffers (initial state uploaded from pinned
+host memory, dt read back every step, final interior downloaded), timed by
+wall clock around synchronised regions.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MHD cell-updates/sec (3 sweeps) at 1/2/4/8 B200; % of HBM/FP64 roofline"
+UNIT = "cell-updates/s"
+HBM_FALLBACK_GBS = 6650.0
+# Algorithmic work per cell-update.
+ALG = {
+    "blast": dict(F=2500.0, B=512.0, F_sweep=(2500.0 - 279.0 - 78.0) / 3.0, B_sweep=128.0),
+    "orszag_tang": dict(F=3330.0, B=512.0, F_sweep=1163.0, B_sweep=128.0),
+    "magnetosphere": dict(F=3910.0, B=608.0, F_sweep=1163.0, B_sweep=152.0),
+    "briowu": dict(F=2500.0, B=512.0, F_sweep=714.0, B_sweep=128.0),
+}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return HBM_FALLBACK_GBS, "fallback"
+
+
+def make_config(name, gpus):
+    from paper_1607_02214_b200 import configs
+    if name == "blast512":
+        return configs.blast(n=512, gpus=gpus), "blast"
+    if name.startswith("blast"):
+        return configs.blast(n=int(name[5:]), gpus=gpus), "blast"
+    if name == "ot512":
+        return configs.orszag_tang(n=512), "orszag_tang"
+    if name == "mag160":
+        return configs.magnetosphere(), "magnetosphere"
+    if name == "mag1024":
+        return configs.magnetosphere(nx=1024, nyz=768, d=0.05, partition=(gpus, 1, 1)), \
+            "magnetosphere"
+    if name == "briowu":
+        return configs.brio_wu(), "briowu"
+    raise SystemExit(f"unknown config {name}")
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index=0):
+        self.dev = device_index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.dev}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        try:
+            for ln in open(self.path):
+                p = [x.strip() for x in ln.split(",")]
+                if len(p) >= 9:
+                    rows.append(p)
+        except Exception:
+            pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i] == "Active"})
+        under = sorted(sm)[len(sm) // 4:] or sm  # drop the idle head of the samples
+        return {"sm_mhz": float(np.median(under)) if under else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(rows)}
+
+
+def fp64_peak_tflops(device=0):
+    import ctypes
+    from paper_1607_02214_b200 import _native as N
+    out = ctypes.c_double()
+    N.check(N.lib.ppmlr_gpu_fp64_peak(device, ctypes.byref(out)))
+    return out.value
+
+
+# ------------------------------------------------------------ CPU baseline
+
+def cpu_baseline(kind_cfg, seconds_target=12.0, threads=None):
+    """The reference's own CPU implementation (oracle/_ref, built from the
+    unmodified sources) on a bounded sample of the workload, one independent
+    harness per host thread.  Falls back to the C restatement ("port")."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle as po
+    threads = threads or os.cpu_count() or 1
+    n = 64
+    specs = [(-0.5, 0.5, -0.5, 0.5, 1.0 / n, n, 1.05)] * 3
+    sample = f"{n}^3 blast unit block (same IC/physics as C4), one independent block per thread"
+    if kind_cfg == "magnetosphere":
+        specs = [(-100.0, 30.0, -10.0, 10.0, 0.4, 160, 1.05),
+                 (-100.0, 100.0, -10.0, 10.0, 0.4, 150, 1.05),
+                 (-100.0, 100.0, -10.0, 10.0, 0.4, 150, 1.05)]
+        sample = "C3 160x150x150 magnetosphere, one independent harness per thread"
+    if po.have_ref():
+        kw = dict(boundary=0) if kind_cfg != "magnetosphere" else dict(boundary=2,
+                                                                       with_dipole=True)
+        ic = (3, (10.0, 0.1, 0.1)) if kind_cfg != "magnetosphere" else (-1, ())
+        # calibrate: one step single-threaded
+        r1, s1 = po.ref_bench(specs, ic[0], ic[1], 1, 1, **kw)
+        steps = max(1, int(seconds_target / max(s1, 1e-3) / 2))
+        rate, secs = po.ref_bench(specs, ic[0], ic[1], threads, steps, **kw)
+        return {"value": rate, "unit": UNIT, "cores": threads, "kind": "reference",
+                "sample": f"{sample}; {steps} steps x {threads} threads in {secs:.1f} s "
+                          f"(oracle/_ref: unmodified reference sources, g++ -O3)"}
+    return cpu_baseline_port(kind_cfg, seconds_target, threads)
+
+
+def cpu_baseline_port(kind_cfg, seconds_target, threads):
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle as po
+    from paper_1607_02214_b200 import configs, host_block_state
+    cfg = configs.blast(n=48)
+    st = host_block_state(cfg.specs, (1, 1, 1), cfg.options, 0, cfg.ic)
+    o = po.opts()
+    c = po.consts()
+    cells = 48 ** 3
+
+    def one(k, out):
+        blk = po.OracleBlock([48] * 3, 4, st["centers"], st["spacings"], [[1, 1]] * 3,
+                             st["fields"].copy())
+        t0 = time.perf_counter()
+        for s in range(k):
+            blk.advance(o, c, s)
+        out.append(time.perf_counter() - t0)
+
+    tmp = []
+    one(1, tmp)
+    steps = max(1, int(seconds_target / max(tmp[0], 1e-3) / 2))
+    res = []
+    ths = [threading.Thread(target=one, args=(steps, res)) for _ in range(threads)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    secs = max(res)
+    return {"value": cells * steps * threads / secs, "unit": UNIT, "cores": threads,
+            "kind": "port", "sample": f"48^3 blast, {steps} steps x {threads} threads "
+                                      "(C restatement oracle/ppmlr_oracle.c)"}
+
+
+# ------------------------------------------------------------ our arm
+
+def bench_single(args):
+    import torch
+    import paper_1607_02214_b200 as P
+    cfg, kind = make_config(args.config, 1)
+    cfg.options.precision = args.precision
+    alg = ALG[kind]
+    cells = cfg.cells
+    torch.cuda.init()
+    peak_fp64 = fp64_peak_tflops(0)
+    hbm, hbm_src = measured_peaks()
+
+    h = P.Harness(cfg.specs, cfg.partition, cfg.options)
+    if cfg.ic[0] == "magnetosphere":
+        h.init_magnetosphere()
+    else:
+        h.init_with(*cfg.ic)
+    blk = h.block(0)
+    stream = torch.cuda.ExternalStream(blk.stream())
+    h.run(args.warmup)
+    blk.synchronize()
+
+    # ---- timed region: K steps, per-sweep CUDA events inside the library
+    blk.timing(True)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(0) as clk:
+        torch.cuda.synchronize()
+        e0.record(stream)
+        h.run(args.steps)
+        e1.record(stream)
+        e1.synchronize()
+    ms = e0.elapsed_time(e1)
+    sweep_ms, kernels, sweep_launches = blk.timing(False)
+    value = cells * args.steps / (ms * 1e-3)
+
+    # ---- dominant kernel roofline (the directional sweep)
+    avg_sweep_s = sweep_ms * 1e-3 / max(sweep_launches, 1)
+    sweep_bytes = cells * alg["B_sweep"]
+    sweep_flops = cells * alg["F_sweep"]
+    frac_hbm = (sweep_bytes / avg_sweep_s) / (hbm * 1e9)
+    frac_fp64 = (sweep_flops / avg_sweep_s) / (peak_fp64 * 1e12)
+    bound = "fp64" if frac_fp64 >= frac_hbm else "hbm"
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_sweep_traffic.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get(args.config, {}).get(args.precision)
+        except Exception:
+            traffic = None
+    roofline = {
+        "bound": bound,
+        "achieved": (sweep_flops / avg_sweep_s / 1e12) if bound == "fp64"
+        else (sweep_bytes / avg_sweep_s / 1e9),
+        "peak": peak_fp64 if bound == "fp64" else hbm,
+        "unit": "TFLOP/s" if bound == "fp64" else "GB/s",
+        "frac": frac_fp64 if bound == "fp64" else frac_hbm,
+        "traffic": traffic,
+        "kernel": "sweep_kernel (x/y/z)",
+        "per_launch": {"cells": cells, "alg_bytes": sweep_bytes, "alg_flops": sweep_flops,
+                       "avg_ms": avg_sweep_s * 1e3, "launches": sweep_launches},
+        "frac_hbm": frac_hbm, "frac_fp64": frac_fp64,
+        "peak_fp64_tflops_measured": peak_fp64, "peak_hbm_gbs": hbm,
+        "peak_hbm_source": hbm_src,
+        "sweep_share_of_step": sweep_ms / ms,
+        # whole step against BASELINE.md §3's roofline formula
+        "step_frac": value / min(hbm * 1e9 / alg["B"], peak_fp64 * 1e12 / alg["F"]),
+    }
+
+    # ---- end to end through the public API with host buffers
+    e2e = bench_e2e(h, cfg, args, cells) if not args.no_e2e else None
+    h.close()
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "precision": args.precision,
+        "data": "synthetic (deterministic IC, no RNG)",
+        "config": {"workload": cfg.name, "grid": [int(s.cells) for s in cfg.specs],
+                   "cells_per_gpu": cells, "partition": "x-slab (P,1,1)",
+                   "l2": "state (2 x 9 GB ping-pong) >> 126 MB L2; no flush needed"},
+        "clocks": clk.summary(), "e2e": e2e, "gpu_launches": int(kernels),
+        "roofline": roofline,
+    }
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(kind)
+    print(json.dumps(line), flush=True)
+
+
+def bench_e2e(h, cfg, args, cells):
+    """K x Harness.advance() (dt read back each step) bracketed by the upload
+    of the initial state from pinned host memory and the download of the
+    final interior into pinned host memory."""
+    import torch
+    import paper_1607_02214_b200 as P
+    st = P.host_block_state(cfg.specs, (1, 1, 1), cfg.options, 0, cfg.ic)
+    host_in = torch.empty(st["fields"].shape, dtype=torch.float64, pin_memory=True).numpy()
+    host_in[...] = st["fields"]
+    nx, ny, nz = (int(s.cells) for s in cfg.specs)
+    host_out = torch.empty((nz, ny, nx, 8), dtype=torch.float64, pin_memory=True).numpy()
+    blk = h.block(0)
+    k = args.steps
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    blk.upload(host_in, st["bd"], st["frozen_idx"], st["frozen_states"])
+    for _ in range(k):
+        h.advance()
+    blk.download_interior(out=host_out)
+    t1 = time.perf_counter()
+    h2d = host_in.nbytes + (st["bd"].nbytes if st["bd"] is not None else 0)
+    d2h = host_out.nbytes + 8 * k
+    return {"value": cells * k / (t1 - t0), "unit": UNIT,
+            "h2d_bytes_per_step": h2d / k, "d2h_bytes_per_step": d2h / k,
+            "how": f"upload(pinned) + {k} x advance() + download_interior(pinned), wall clock"}
+
+
+def bench_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    _, kind = make_config(args.config, 1) if args.config != "mag1024" else (None,
+                                                                           "magnetosphere")
+    cb = cpu_baseline(kind, seconds_target=max(6.0, 2.0 * args.steps))
+    line = {"metric": METRIC, "value": cb["value"], "unit": UNIT, "impl": "reference",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": args.config},
+            "cpu_baseline": cb,
+            "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="blast512")
+    ap.add_argument("--precision", default="strict", choices=["strict", "fast"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return bench_reference(args)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1 or args.gpus > 1:
+        from paper_1607_02214_b200 import dist
+        return dist.bench_distributed(args, METRIC, UNIT, ALG, make_config, ClockSampler,
+                                      fp64_peak_tflops, measured_peaks, cpu_baseline)
+    return bench_single(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,1482 @@
+// Device-resident block: state upload/download, boundary fills, CFL
+// reduction, dipole source terms, frozen core, halo pack/unpack and the
+// per-step CUDA graph.  Compiled with --fmad=false so every arithmetic
+// kernel here is bit-identical to the reference (proj/src/stepper.cpp).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <limits>
+#include <string>
+#include <vector>
+
+#include "block.hpp"
+#include "sweep.cuh"
+
+using namespace ppmlr_b200;
+using namespace ppmlr_b200::strict;
+
+namespace ppmlr_b200 {
+
+thread_local std::string g_last_error;
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+int cuda_fail(cudaError_t e, const char* where) {
+  set_error(std::string("CUDA error in ") + where + ": " + cudaGetErrorString(e));
+  return PPMLR_RUNTIME;
+}
+
+}  // namespace ppmlr_b200
+
+#define CK(call)                                              \
+  do {                                                        \
+    cudaError_t e_ = (call);                                  \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call);       \
+  } while (0)
+
+namespace {
+
+constexpr unsigned long long kInfBits = 0x7FF0000000000000ull;
+
+// ------------------------------------------------------------------ layout
+
+struct Lay {
+  int n0, n1, n2;
+  int P0, S1;
+  long long sy, sz, ncell;
+  __host__ __device__ long long idx(int i, int j, int k) const {  // interior coords
+    return (long long)(i + kG) + sy * (j + kG) + sz * (k + kG);
+  }
+};
+
+Lay lay_of(const ppmlr_gpu_block* b) {
+  Lay l;
+  l.n0 = b->n[0];
+  l.n1 = b->n[1];
+  l.n2 = b->n[2];
+  l.P0 = b->P0;
+  l.S1 = b->S[1];
+  l.sy = b->sy;
+  l.sz = b->sz;
+  l.ncell = b->ncell;
+  return l;
+}
+
+struct Planes {
+  double* f[8];
+};
+Planes planes(double* base, long long ncell) {
+  Planes p;
+  for (int f = 0; f < 8; ++f) p.f[f] = base + f * ncell;
+  return p;
+}
+
+// ---------------------------------------------------------------- kernels
+
+// Reference AoS (ghost gr) k-plane chunk -> device SoA (ghost 4).
+__global__ void aos_to_soa_kernel(const double* __restrict__ aos, int nper, Planes dst, Lay L,
+                                  int gr, int S0r, int S1r, int kr0, int nk, const double* bdsrc,
+                                  double* bd0, double* bd1, double* bd2) {
+  const long long total = (long long)S0r * S1r * nk;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int ir = (int)(t % S0r);
+    const int jr = (int)((t / S0r) % S1r);
+    const int kr = kr0 + (int)(t / ((long long)S0r * S1r));
+    const int i = ir - gr, j = jr - gr, k = kr - gr;
+    if (i < -kG || i >= L.n0 + kG || j < -kG || j >= L.n1 + kG || k < -kG || k >= L.n2 + kG)
+      continue;
+    const long long d = L.idx(i, j, k);
+    if (aos) {
+      const double* s = aos + t * nper;
+      for (int f = 0; f < 8; ++f) dst.f[f][d] = s[f];
+    }
+    if (bdsrc) {
+      const double* s = bdsrc + t * 3;
+      bd0[d] = s[0];
+      bd1[d] = s[1];
+      bd2[d] = s[2];
+    }
+  }
+}
+
+// Device SoA -> reference AoS (ghost gr) k-plane chunk.
+__global__ void soa_to_aos_kernel(double* __restrict__ aos, Planes src, Lay L, int gr, int S0r,
+                                  int S1r, int kr0, int nk) {
+  const long long total = (long long)S0r * S1r * nk;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int ir = (int)(t % S0r);
+    const int jr = (int)((t / S0r) % S1r);
+    const int kr = kr0 + (int)(t / ((long long)S0r * S1r));
+    const int i = ir - gr, j = jr - gr, k = kr - gr;
+    double* o = aos + t * 8;
+    if (i < -kG || i >= L.n0 + kG || j < -kG || j >= L.n1 + kG || k < -kG || k >= L.n2 + kG) {
+      for (int f = 0; f < 8; ++f) o[f] = 0.0;
+      continue;
+    }
+    const long long d = L.idx(i, j, k);
+    for (int f = 0; f < 8; ++f) o[f] = src.f[f][d];
+  }
+}
+
+// Interior only, x fastest.
+__global__ void soa_to_interior_kernel(double* __restrict__ out, Planes src, Lay L) {
+  const long long total = (long long)L.n0 * L.n1 * L.n2;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(t % L.n0);
+    const int j = (int)((t / L.n0) % L.n1);
+    const int k = (int)(t / ((long long)L.n0 * L.n1));
+    const long long d = L.idx(i, j, k);
+    for (int f = 0; f < 8; ++f) out[t * 8 + f] = src.f[f][d];
+  }
+}
+
+// apply_boundaries (stepper.cpp:202-247) for one axis, `layers` ghost layers,
+// over the interior transverse span.  mode: 0 outflow, 1 periodic,
+// 2 magnetosphere (the sunward +x shell is constant and pre-filled).
+__global__ void bc_kernel(Planes s, Lay L, int axis, int phys_lo, int phys_hi, int layers,
+                          int mode) {
+  const int na = axis == 0 ? L.n0 : (axis == 1 ? L.n1 : L.n2);
+  const int nb = axis == 0 ? L.n1 : (axis == 1 ? L.n2 : L.n0);
+  const int nc = axis == 0 ? L.n2 : (axis == 1 ? L.n0 : L.n1);
+  const long long per_side = (long long)layers * nb * nc;
+  const long long total = 2 * per_side;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int side = (int)(t / per_side);
+    const long long r = t - side * per_side;
+    // layer fastest for axis 0 (contiguous), transverse fastest otherwise
+    int layer, t1, t2;
+    if (axis == 0) {
+      layer = 1 + (int)(r % layers);
+      t1 = (int)((r / layers) % nb);
+      t2 = (int)(r / ((long long)layers * nb));
+    } else {
+      // iterate x fastest: for axis 1, x = t2 (d axis); for axis 2, x = t1 (b axis)
+      if (axis == 1) {
+        t2 = (int)(r % nc);
+        t1 = (int)((r / nc) % nb);
+        layer = 1 + (int)(r / ((long long)nc * nb));
+      } else {
+        t1 = (int)(r % nb);
+        t2 = (int)((r / nb) % nc);
+        layer = 1 + (int)(r / ((long long)nb * nc));
+      }
+    }
+    if (side == 0 && !phys_lo) continue;
+    if (side == 1 && !phys_hi) continue;
+    if (mode == 2 && axis == 0 && side == 1) continue;  // sunward inflow: pre-filled
+    int cell[3], src[3];
+    cell[(axis + 1) % 3] = src[(axis + 1) % 3] = t1;
+    cell[(axis + 2) % 3] = src[(axis + 2) % 3] = t2;
+    cell[axis] = side == 0 ? -layer : na - 1 + layer;
+    if (mode == 1)
+      src[axis] = side == 0 ? na - layer : layer - 1;
+    else
+      src[axis] = side == 0 ? 0 : na - 1;
+    const long long d = L.idx(cell[0], cell[1], cell[2]);
+    const long long q = L.idx(src[0], src[1], src[2]);
+#pragma unroll
+    for (int f = 0; f < 8; ++f) s.f[f][d] = s.f[f][q];
+  }
+}
+
+// Sunward (+x) ghost shell in Magnetosphere mode: rho, v, p of the wind and
+// B' = imf - bd(ghost)  (stepper.cpp:227-236).  Constant for the whole run.
+__global__ void wind_fill_kernel(Planes s, Lay L, const double* bd0, const double* bd1,
+                                 const double* bd2, double rho, double p, double v0, double v1,
+                                 double v2, double i0, double i1, double i2) {
+  const long long total = (long long)kG * L.n1 * L.n2;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int layer = 1 + (int)(t % kG);
+    const int j = (int)((t / kG) % L.n1);
+    const int k = (int)(t / ((long long)kG * L.n1));
+    const long long d = L.idx(L.n0 - 1 + layer, j, k);
+    s.f[0][d] = rho;
+    s.f[1][d] = v0;
+    s.f[2][d] = v1;
+    s.f[3][d] = v2;
+    s.f[4][d] = i0 - (bd0 ? bd0[d] : 0.0);
+    s.f[5][d] = i1 - (bd1 ? bd1[d] : 0.0);
+    s.f[6][d] = i2 - (bd2 ? bd2[d] : 0.0);
+    s.f[7][d] = p;
+  }
+}
+
+struct CtxPtrs {
+  unsigned long long* err;
+  unsigned long long* step;
+  unsigned long long* min;
+  double* dt;
+  double* dt_prev;
+  double* time;
+};
+
+// The three CFL candidates of compute_dt (stepper.cpp:128-137) for one cell.
+// Returns false (and the failing axis) on a non-finite candidate.
+__device__ __forceinline__ bool cfl_cell(const double* s, double b0, double b1, double b2,
+                                         double d0, double d1, double d2, const Consts& c,
+                                         double& mn, int& bad_axis) {
+  const double cand0 = d0 / (fabs(s[1]) + fast_speed3<0>(s, b0, b1, b2, c));
+  if (!isfinite(cand0)) {
+    bad_axis = 0;
+    return false;
+  }
+  const double cand1 = d1 / (fabs(s[2]) + fast_speed3<1>(s, b0, b1, b2, c));
+  if (!isfinite(cand1)) {
+    bad_axis = 1;
+    return false;
+  }
+  const double cand2 = d2 / (fabs(s[3]) + fast_speed3<2>(s, b0, b1, b2, c));
+  if (!isfinite(cand2)) {
+    bad_axis = 2;
+    return false;
+  }
+  mn = smin(smin(smin(mn, cand0), cand1), cand2);
+  return true;
+}
+
+__device__ __forceinline__ void block_min_commit(double mn, unsigned long long* gmin) {
+  // positive doubles order like their bit patterns
+  unsigned long long bits = __double_as_longlong(mn);
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long other = __shfl_xor_sync(0xffffffffu, bits, o);
+    bits = other < bits ? other : bits;
+  }
+  __shared__ unsigned long long wmin[32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) wmin[w] = bits;
+  __syncthreads();
+  if (w == 0) {
+    const int nw = (blockDim.x + 31) >> 5;
+    bits = lane < nw ? wmin[lane] : kInfBits;
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long other = __shfl_xor_sync(0xffffffffu, bits, o);
+      bits = other < bits ? other : bits;
+    }
+    if (lane == 0 && bits != kInfBits) atomicMin(gmin, bits);
+  }
+}
+
+// Standalone compute_dt over the interior; min into ctx.min.
+template <bool DIPOLE>
+__global__ void cfl_kernel(Planes s, Lay L, const double* bd0, const double* bd1,
+                           const double* bd2, const double* dx0, const double* dx1,
+                           const double* dx2, Consts c, CtxPtrs ctx, unsigned long long step_add) {
+  const long long total = (long long)L.n0 * L.n1 * L.n2;
+  double mn = __longlong_as_double(kInfBits);
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(t % L.n0);
+    const int j = (int)((t / L.n0) % L.n1);
+    const int k = (int)(t / ((long long)L.n0 * L.n1));
+    const long long d = L.idx(i, j, k);
+    double q[8];
+#pragma unroll
+    for (int f = 0; f < 8; ++f) q[f] = s.f[f][d];
+    int bad = 0;
+    if (!cfl_cell(q, DIPOLE ? bd0[d] : 0.0, DIPOLE ? bd1[d] : 0.0, DIPOLE ? bd2[d] : 0.0,
+                  dx0[i + kG], dx1[j + kG], dx2[k + kG], c, mn, bad))
+      atomicMin(ctx.err, err_key(*ctx.step + step_add, kPhaseCfl, 0,
+                                 ((unsigned long long)t * 3 + bad) << 2));
+  }
+  block_min_commit(mn, ctx.min);
+}
+
+// dt = cfl * min; optionally close the current step first.
+__global__ void step_end_kernel(CtxPtrs ctx, double cfl, int close_step, int have_min) {
+  if (close_step) {
+    *ctx.time += *ctx.dt;
+    *ctx.dt_prev = *ctx.dt;
+    *ctx.step += 1;
+  }
+  if (have_min) {
+    *ctx.dt = cfl * __longlong_as_double(*ctx.min);
+    *ctx.min = kInfBits;
+  }
+}
+
+__device__ __forceinline__ double central_diff(double fm, double f0, double fp, double hm,
+                                               double hp) {
+  return (((hm * hm) * fp + ((hp * hp) - (hm * hm)) * f0) - (hp * hp) * fm) /
+         ((hm * hp) * (hm + hp));
+}
+
+__device__ __forceinline__ void cross3(double ax, double ay, double az, double bx, double by,
+                                       double bz, double* o) {
+  o[0] = ay * bz - az * by;
+  o[1] = az * bx - ax * bz;
+  o[2] = ax * by - ay * bx;
+}
+
+struct SrcArgs {
+  Planes in, out;
+  Lay L;
+  const double *bd0, *bd1, *bd2;
+  const double *hm0, *hp0, *hm1, *hp1, *hm2, *hp2;  // per axis, ghost-inclusive
+  const double *dx0, *dx1, *dx2;
+  // frozen core
+  int fl0, fl1, fl2, fn0, fn1, fn2;
+  const int* fslot;
+  const double* fst;
+  long long nfrozen;
+  Consts c;
+  CtxPtrs ctx;
+  int fuse_cfl;
+};
+
+// apply_sources (stepper.cpp:141-200) + restore_frozen_core (:284-286) +
+// the next step's compute_dt (:119-139), one thread per interior cell.
+template <bool DIPOLE>
+__global__ void sources_kernel(const SrcArgs A) {
+  const Lay& L = A.L;
+  const Consts& c = A.c;
+  const long long total = (long long)L.n0 * L.n1 * L.n2;
+  double mn = __longlong_as_double(kInfBits);
+  const unsigned long long step = *A.ctx.step;
+  const double dt = *A.ctx.dt;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(t % L.n0);
+    const int j = (int)((t / L.n0) % L.n1);
+    const int k = (int)(t / ((long long)L.n0 * L.n1));
+    const long long d = L.idx(i, j, k);
+    double s[8];
+#pragma unroll
+    for (int f = 0; f < 8; ++f) s[f] = A.in.f[f][d];
+    const double b0 = DIPOLE ? A.bd0[d] : 0.0, b1 = DIPOLE ? A.bd1[d] : 0.0,
+                 b2 = DIPOLE ? A.bd2[d] : 0.0;
+    double gb[3][3], ge[3][3];
+    double e0[3];
+    cross3(s[1], s[2], s[3], b0, b1, b2, e0);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const long long st = a == 0 ? 1 : (a == 1 ? L.sy : L.sz);
+      const long long dm = d - st, dp = d + st;
+      const int lc = (a == 0 ? i : (a == 1 ? j : k)) + kG;
+      const double hm = (a == 0 ? A.hm0 : (a == 1 ? A.hm1 : A.hm2))[lc];
+      const double hp = (a == 0 ? A.hp0 : (a == 1 ? A.hp1 : A.hp2))[lc];
+      double em[3], ep[3];
+      cross3(A.in.f[1][dm], A.in.f[2][dm], A.in.f[3][dm], DIPOLE ? A.bd0[dm] : 0.0,
+             DIPOLE ? A.bd1[dm] : 0.0, DIPOLE ? A.bd2[dm] : 0.0, em);
+      cross3(A.in.f[1][dp], A.in.f[2][dp], A.in.f[3][dp], DIPOLE ? A.bd0[dp] : 0.0,
+             DIPOLE ? A.bd1[dp] : 0.0, DIPOLE ? A.bd2[dp] : 0.0, ep);
+#pragma unroll
+      for (int comp = 0; comp < 3; ++comp) {
+        gb[a][comp] = central_diff(A.in.f[4 + comp][dm], s[4 + comp], A.in.f[4 + comp][dp], hm, hp);
+        ge[a][comp] = central_diff(em[comp], e0[comp], ep[comp], hm, hp);
+      }
+    }
+    const double cb0 = gb[1][2] - gb[2][1], cb1 = gb[2][0] - gb[0][2], cb2 = gb[0][1] - gb[1][0];
+    const double ce0 = ge[1][2] - ge[2][1], ce1 = ge[2][0] - ge[0][2], ce2 = ge[0][1] - ge[1][0];
+    const double div_b = (gb[0][0] + gb[1][1]) + gb[2][2];
+    double sm[3];
+    cross3(cb0, cb1, cb2, b0, b1, b2, sm);
+    sm[0] = sm[0] / c.mu0;
+    sm[1] = sm[1] / c.mu0;
+    sm[2] = sm[2] / c.mu0;
+    const double si0 = ce0 - s[1] * div_b, si1 = ce1 - s[2] * div_b, si2 = ce2 - s[3] * div_b;
+    const double se = ((s[1] * sm[0] + s[2] * sm[1]) + s[3] * sm[2]) +
+                      ((s[4] * ce0 + s[5] * ce1) + s[6] * ce2) / c.mu0;
+    double u[8];
+    prim_to_cons3(s, u, c);
+    u[1] = u[1] + sm[0] * dt;
+    u[2] = u[2] + sm[1] * dt;
+    u[3] = u[3] + sm[2] * dt;
+    u[4] = u[4] + si0 * dt;
+    u[5] = u[5] + si1 * dt;
+    u[6] = u[6] + si2 * dt;
+    u[7] = u[7] + dt * se;
+    double q[8];
+    const int bad = cons_to_prim3(u, q, c);
+    if (bad) {
+      atomicMin(A.ctx.err, err_key(step, kPhaseSources, 0,
+                                   ((unsigned long long)t << 2) |
+                                       (bad == 1 ? kErrDensity : kErrPressure)));
+#pragma unroll
+      for (int f = 0; f < 8; ++f) q[f] = s[f];
+    }
+    // frozen inner core overrides the update (restore_frozen_core)
+    if (A.nfrozen > 0) {
+      const int fi = i - A.fl0, fj = j - A.fl1, fk = k - A.fl2;
+      if (fi >= 0 && fi < A.fn0 && fj >= 0 && fj < A.fn1 && fk >= 0 && fk < A.fn2) {
+        const int slot = A.fslot[fi + A.fn0 * (fj + A.fn1 * fk)];
+        if (slot >= 0) {
+#pragma unroll
+          for (int f = 0; f < 8; ++f) q[f] = A.fst[f * A.nfrozen + slot];
+        }
+      }
+    }
+#pragma unroll
+    for (int f = 0; f < 8; ++f) A.out.f[f][d] = q[f];
+    if (A.fuse_cfl) {
+      int badax = 0;
+      if (!cfl_cell(q, b0, b1, b2, A.dx0[i + kG], A.dx1[j + kG], A.dx2[k + kG], c, mn, badax))
+        atomicMin(A.ctx.err, err_key(step + 1, kPhaseCfl, 0, ((unsigned long long)t * 3 + badax) << 2));
+    }
+  }
+  if (A.fuse_cfl) block_min_commit(mn, A.ctx.min);
+}
+
+__global__ void frozen_restore_kernel(Planes s, const long long* idx, const double* st,
+                                      long long nf) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nf;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long d = idx[t];
+#pragma unroll
+    for (int f = 0; f < 8; ++f) s.f[f][d] = st[f * nf + t];
+  }
+}
+
+// Face slab addressing (exchange.cpp:17-27): layer q of the face in global
+// order; pack order t2 -> t1 -> layer -> 8 scalars.
+__device__ __forceinline__ void face_cell(int axis, int t1, int t2, int along, int* cell) {
+  cell[(axis + 1) % 3] = t1;
+  cell[(axis + 2) % 3] = t2;
+  cell[axis] = along;
+}
+
+__global__ void pack_kernel(Planes s, Lay L, int face, int layers, double* out) {
+  const int axis = face / 2;
+  const int na = axis == 0 ? L.n0 : (axis == 1 ? L.n1 : L.n2);
+  const int nb = axis == 0 ? L.n1 : (axis == 1 ? L.n2 : L.n0);
+  const int nc = axis == 0 ? L.n2 : (axis == 1 ? L.n0 : L.n1);
+  const long long total = (long long)nb * nc * layers;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int q = (int)(t % layers);
+    const int t1 = (int)((t / layers) % nb);
+    const int t2 = (int)(t / ((long long)layers * nb));
+    int cell[3];
+    face_cell(axis, t1, t2, face % 2 == 0 ? q : na - layers + q, cell);
+    const long long d = L.idx(cell[0], cell[1], cell[2]);
+#pragma unroll
+    for (int f = 0; f < 8; ++f) out[t * 8 + f] = s.f[f][d];
+  }
+}
+
+// `face` is the receiver's face; the slab came from the sender's opposite face.
+__global__ void unpack_kernel(Planes s, Lay L, int face, int layers, const double* in) {
+  const int axis = face / 2;
+  const int na = axis == 0 ? L.n0 : (axis == 1 ? L.n1 : L.n2);
+  const int nb = axis == 0 ? L.n1 : (axis == 1 ? L.n2 : L.n0);
+  const int nc = axis == 0 ? L.n2 : (axis == 1 ? L.n0 : L.n1);
+  const int src_face = face ^ 1;
+  const long long total = (long long)nb * nc * layers;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int q = (int)(t % layers);
+    const int t1 = (int)((t / layers) % nb);
+    const int t2 = (int)(t / ((long long)layers * nb));
+    int cell[3];
+    face_cell(axis, t1, t2, src_face % 2 == 0 ? na + q : -layers + q, cell);
+    const long long d = L.idx(cell[0], cell[1], cell[2]);
+#pragma unroll
+    for (int f = 0; f < 8; ++f) s.f[f][d] = in[t * 8 + f];
+  }
+}
+
+__global__ void copy_face_kernel(Planes dst, Lay Ld, Planes src, Lay Ls, int face, int layers) {
+  const int axis = face / 2;
+  const int nad = axis == 0 ? Ld.n0 : (axis == 1 ? Ld.n1 : Ld.n2);
+  const int nas = axis == 0 ? Ls.n0 : (axis == 1 ? Ls.n1 : Ls.n2);
+  const int nb = axis == 0 ? Ld.n1 : (axis == 1 ? Ld.n2 : Ld.n0);
+  const int nc = axis == 0 ? Ld.n2 : (axis == 1 ? Ld.n0 : Ld.n1);
+  const int src_face = face ^ 1;
+  const long long total = (long long)nb * nc * layers;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int q = (int)(t % layers);
+    const int t1 = (int)((t / layers) % nb);
+    const int t2 = (int)(t / ((long long)layers * nb));
+    int cs[3], cd[3];
+    face_cell(axis, t1, t2, src_face % 2 == 0 ? q : nas - layers + q, cs);
+    face_cell(axis, t1, t2, src_face % 2 == 0 ? nad + q : -layers + q, cd);
+    const long long ds = Ls.idx(cs[0], cs[1], cs[2]);
+    const long long dd = Ld.idx(cd[0], cd[1], cd[2]);
+#pragma unroll
+    for (int f = 0; f < 8; ++f) dst.f[f][dd] = src.f[f][ds];
+  }
+}
+
+int grid_for(long long work, int threads = 256) {
+  long long g = (work + threads - 1) / threads;
+  if (g < 1) g = 1;
+  if (g > 148 * 32) g = 148 * 32;
+  return (int)g;
+}
+
+// ----------------------------------------------------------- host helpers
+
+CtxPtrs ctx_of(ppmlr_gpu_block* b) {
+  return CtxPtrs{b->d_err, b->d_step, b->d_min, b->d_dt, b->d_dt_prev, b->d_time};
+}
+
+double* cur_buf(ppmlr_gpu_block* b) { return b->buf[b->cur]; }
+
+// Reference message for a decoded error key (sweep / sources / CFL).
+int decode_error(ppmlr_gpu_block* b, unsigned long long key, std::string& msg) {
+  const int phase = (int)((key >> 43) & 7);
+  const unsigned long long pos = key & ((1ull << 41) - 1);
+  const int kind = (int)(pos & 3);
+  char buf[512];
+  if (phase == kPhaseCfl) {
+    const unsigned long long cell = (pos >> 2) / 3;
+    const int i = (int)(cell % b->n[0]);
+    const int j = (int)((cell / b->n[0]) % b->n[1]);
+    const int k = (int)(cell / ((unsigned long long)b->n[0] * b->n[1]));
+    std::snprintf(buf, sizeof buf, "non-finite signal speed at cell (%d,%d,%d)", i, j, k);
+    msg = buf;
+    return PPMLR_UNPHYSICAL;
+  }
+  if (phase == kPhaseSources) {
+    const unsigned long long cell = pos >> 2;
+    const int i = (int)(cell % b->n[0]);
+    const int j = (int)((cell / b->n[0]) % b->n[1]);
+    const int k = (int)(cell / ((unsigned long long)b->n[0] * b->n[1]));
+    std::snprintf(buf, sizeof buf, "%s after sources at cell (%d,%d,%d)",
+                  kind == kErrDensity ? "non-positive density"
+                                      : "non-positive pressure recovered from conserved state",
+                  i, j, k);
+    msg = buf;
+    return PPMLR_UNPHYSICAL;
+  }
+  const int axis = (int)((key >> 41) & 3);
+  const unsigned long long pencil = pos >> 20;
+  const int sub = (int)((pos >> 19) & 1);
+  const int zone = (int)((pos >> 2) & 0x1FFFF);
+  const int nb = b->n[(axis + 1) % 3];
+  const int t1 = (int)(pencil % nb), t2 = (int)(pencil / nb);
+  if (sub == 0) {
+    if (kind == kErrStepRejected)
+      std::snprintf(buf, sizeof buf, "Lagrangian interfaces crossed at zone %d", zone);
+    else
+      std::snprintf(buf, sizeof buf,
+                    "negative density or pressure after Lagrangian step at zone %d", zone);
+  } else {
+    std::snprintf(buf, sizeof buf, "%s at strip cell %d",
+                  kind == kErrDensity ? "non-positive density"
+                                      : "non-positive pressure recovered from conserved state",
+                  zone);
+  }
+  msg = buf;
+  std::snprintf(buf, sizeof buf, " in sweep axis %d at line (%d,%d)", axis, t1, t2);
+  msg += buf;
+  return PPMLR_UNPHYSICAL;  // stepper.cpp:272-276 rethrows as UnphysicalState
+}
+
+void build_axis_tables(const std::vector<double>& dx, const std::vector<double>& ce,
+                       std::vector<double>& slope, std::vector<double>& qfc,
+                       std::vector<double>& hm, std::vector<double>& hp) {
+  const int nn = (int)dx.size();
+  slope.assign(3 * nn, 0.0);
+  qfc.assign(5 * (nn + 1), 0.0);
+  hm.assign(nn, 0.0);
+  hp.assign(nn, 0.0);
+  for (int k = 1; k + 1 < nn; ++k) {
+    slope[3 * k] = dx[k] / ((dx[k - 1] + dx[k]) + dx[k + 1]);
+    slope[3 * k + 1] = (2.0 * dx[k - 1] + dx[k]) / (dx[k + 1] + dx[k]);
+    slope[3 * k + 2] = (dx[k] + 2.0 * dx[k + 1]) / (dx[k - 1] + dx[k]);
+  }
+  for (int m = 2; m + 1 < nn; ++m) {
+    const int i = m - 1;
+    double* e = &qfc[5 * m];
+    e[0] = dx[i] / (dx[i] + dx[i + 1]);
+    e[1] = 1.0 / (((dx[i - 1] + dx[i]) + dx[i + 1]) + dx[i + 2]);
+    e[2] = (((2.0 * dx[i + 1]) * dx[i]) / (dx[i] + dx[i + 1])) *
+           ((dx[i - 1] + dx[i]) / (2.0 * dx[i] + dx[i + 1]) -
+            (dx[i + 2] + dx[i + 1]) / (2.0 * dx[i + 1] + dx[i]));
+    e[3] = (dx[i] * (dx[i - 1] + dx[i])) / (2.0 * dx[i] + dx[i + 1]);
+    e[4] = (dx[i + 1] * (dx[i + 1] + dx[i + 2])) / (dx[i] + 2.0 * dx[i + 1]);
+  }
+  for (int l = 1; l < nn; ++l) hm[l] = ce[l] - ce[l - 1];
+  for (int l = 0; l + 1 < nn; ++l) hp[l] = ce[l + 1] - ce[l];
+}
+
+template <typename T>
+int upload_vec(T** dst, const std::vector<T>& v) {
+  CK(cudaMalloc(dst, sizeof(T) * std::max<size_t>(v.size(), 1)));
+  CK(cudaMemcpy(*dst, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice));
+  return 0;
+}
+
+int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v ? std::atoi(v) : dflt;
+}
+
+void choose_sweep_tiles(ppmlr_gpu_block* b) {
+  const int Lmax = env_int("PPMLR_SWEEP_LMAX", 120);
+  const int ipt = env_int("PPMLR_SWEEP_IPT", 2);
+  for (int a = 0; a < 3; ++a) {
+    const int n = b->n[a];
+    const int nseg = (n + Lmax - 1) / Lmax;
+    const int L = (n + nseg - 1) / nseg;
+    b->sweep_L[a] = L;
+    const int T = 4 * (L + 8);
+    int nt = (T + ipt - 1) / ipt;
+    nt = ((nt + 31) / 32) * 32;
+    b->sweep_threads[a] = std::min(512, std::max(32, nt));
+  }
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ sweeps
+
+namespace ppmlr_b200 {
+
+int launch_sweep(ppmlr_gpu_block* b, int axis, int phase) {
+  SweepArgs A;
+  double* in = b->buf[b->cur];
+  double* out = b->buf[b->cur ^ 1];
+  for (int f = 0; f < 8; ++f) {
+    A.src[f] = in + f * b->ncell;
+    A.dst[f] = out + f * b->ncell;
+  }
+  for (int k = 0; k < 3; ++k) A.bd[k] = b->bd ? b->bd + k * b->ncell : nullptr;
+  A.dx = b->ax[axis].dx;
+  A.slope = b->ax[axis].slope;
+  A.qfc = b->ax[axis].qfc;
+  const long long strides[3] = {1, b->sy, b->sz};
+  const int G = axis == 0 ? 1 : 0;
+  const int O = axis == 2 ? 1 : 2;
+  A.stride_a = strides[axis];
+  A.stride_g = strides[G];
+  A.stride_o = strides[O];
+  A.n = b->n[axis];
+  A.ng = b->n[G];
+  A.no = b->n[O];
+  A.nb = b->n[(axis + 1) % 3];
+  A.L = b->sweep_L[axis];
+  A.nseg = (A.n + A.L - 1) / A.L;
+  A.ngroups = (A.ng + 3) / 4;
+  A.dt = b->d_dt;
+  A.err = b->d_err;
+  A.step = b->d_step;
+  A.phase = phase;
+  A.c = b->c;
+  const int T = 4 * (A.L + 8);
+  const size_t smem = sizeof(double) * (size_t)T * (33 + (b->with_dipole ? 3 : 0));
+  // The sweep writes only the interior of the output buffer; its ghost
+  // shells stay stale until the next fill (every reader fills first).
+  cudaError_t e = b->precision == PPMLR_FAST
+                      ? launch_sweep_fast(axis, b->with_dipole, A, b->sweep_threads[axis], smem,
+                                          b->stream)
+                      : launch_sweep_strict(axis, b->with_dipole, A, b->sweep_threads[axis],
+                                            smem, b->stream);
+  if (e != cudaSuccess) return cuda_fail(e, "sweep kernel launch");
+  b->kernel_launches += 1;
+  b->cur ^= 1;
+  return 0;
+}
+
+int launch_bc(ppmlr_gpu_block* b, int axis_mask, int layers) {
+  const Lay L = lay_of(b);
+  Planes s = planes(cur_buf(b), b->ncell);
+  for (int a = 0; a < 3; ++a) {
+    if (!(axis_mask & (1 << a))) continue;
+    if (!b->physical[a][0] && !b->physical[a][1]) continue;
+    const long long work = 2LL * layers * b->n[(a + 1) % 3] * b->n[(a + 2) % 3];
+    bc_kernel<<<grid_for(work), 256, 0, b->stream>>>(s, L, a, b->physical[a][0],
+                                                      b->physical[a][1], layers, b->boundary);
+    b->kernel_launches += 1;
+  }
+  CK(cudaGetLastError());
+  return 0;
+}
+
+int launch_cfl(ppmlr_gpu_block* b, unsigned long long step_add) {
+  const Lay L = lay_of(b);
+  Planes s = planes(cur_buf(b), b->ncell);
+  const long long work = (long long)b->n[0] * b->n[1] * b->n[2];
+  const double* bd0 = b->bd ? b->bd : nullptr;
+  const double* bd1 = b->bd ? b->bd + b->ncell : nullptr;
+  const double* bd2 = b->bd ? b->bd + 2 * b->ncell : nullptr;
+  if (b->with_dipole)
+    cfl_kernel<true><<<grid_for(work), 256, 0, b->stream>>>(s, L, bd0, bd1, bd2, b->ax[0].dx,
+                                                             b->ax[1].dx, b->ax[2].dx, b->c,
+                                                             ctx_of(b), step_add);
+  else
+    cfl_kernel<false><<<grid_for(work), 256, 0, b->stream>>>(s, L, bd0, bd1, bd2, b->ax[0].dx,
+                                                              b->ax[1].dx, b->ax[2].dx, b->c,
+                                                              ctx_of(b), step_add);
+  CK(cudaGetLastError());
+  b->kernel_launches += 1;
+  return 0;
+}
+
+int launch_sources(ppmlr_gpu_block* b, int fuse_cfl) {
+  SrcArgs A;
+  A.in = planes(b->buf[b->cur], b->ncell);
+  A.out = planes(b->buf[b->cur ^ 1], b->ncell);
+  A.L = lay_of(b);
+  A.bd0 = b->bd ? b->bd : nullptr;
+  A.bd1 = b->bd ? b->bd + b->ncell : nullptr;
+  A.bd2 = b->bd ? b->bd + 2 * b->ncell : nullptr;
+  A.hm0 = b->ax[0].hm;
+  A.hp0 = b->ax[0].hp;
+  A.hm1 = b->ax[1].hm;
+  A.hp1 = b->ax[1].hp;
+  A.hm2 = b->ax[2].hm;
+  A.hp2 = b->ax[2].hp;
+  A.dx0 = b->ax[0].dx;
+  A.dx1 = b->ax[1].dx;
+  A.dx2 = b->ax[2].dx;
+  A.fl0 = b->fbox_lo[0];
+  A.fl1 = b->fbox_lo[1];
+  A.fl2 = b->fbox_lo[2];
+  A.fn0 = b->fbox_n[0];
+  A.fn1 = b->fbox_n[1];
+  A.fn2 = b->fbox_n[2];
+  A.fslot = b->fslot;
+  A.fst = b->fstates;
+  A.nfrozen = b->n_frozen;
+  A.c = b->c;
+  A.ctx = ctx_of(b);
+  A.fuse_cfl = fuse_cfl;
+  const long long work = (long long)b->n[0] * b->n[1] * b->n[2];
+  if (b->with_dipole)
+    sources_kernel<true><<<grid_for(work), 256, 0, b->stream>>>(A);
+  else
+    sources_kernel<false><<<grid_for(work), 256, 0, b->stream>>>(A);
+  CK(cudaGetLastError());
+  b->kernel_launches += 1;
+  b->cur ^= 1;
+  return 0;
+}
+
+int launch_frozen(ppmlr_gpu_block* b) {
+  if (b->n_frozen <= 0) return 0;
+  frozen_restore_kernel<<<grid_for(b->n_frozen), 256, 0, b->stream>>>(
+      planes(cur_buf(b), b->ncell), b->fidx, b->fstates, b->n_frozen);
+  CK(cudaGetLastError());
+  b->kernel_launches += 1;
+  return 0;
+}
+
+int launch_step_end(ppmlr_gpu_block* b, double cfl, int close_step, int have_min) {
+  step_end_kernel<<<1, 1, 0, b->stream>>>(ctx_of(b), cfl, close_step, have_min);
+  CK(cudaGetLastError());
+  b->kernel_launches += 1;
+  return 0;
+}
+
+}  // namespace ppmlr_b200
+
+namespace ppmlr_b200 {
+int block_set_dt(ppmlr_gpu_block* b, double dt) {
+  if (dt < 0.0) return 0;  // use the device slot as is
+  b->h_pinned[1] = dt;
+  CK(cudaMemcpyAsync(b->d_dt, &b->h_pinned[1], 8, cudaMemcpyHostToDevice, b->stream));
+  return 0;
+}
+}  // namespace ppmlr_b200
+
+// ---------------------------------------------------------------- C-ABI
+
+extern "C" {
+
+const char* ppmlr_gpu_last_error(void) { return g_last_error.c_str(); }
+
+const char* ppmlr_gpu_version(void) {
+  return "ppmlr-b200 0.1 (sm_100a, FP64 PPMLR sweeps; strict+fast)";
+}
+
+int ppmlr_gpu_block_create(const ppmlr_gpu_block_desc* d, ppmlr_gpu_block** out) {
+  *out = nullptr;
+  if (!d) {
+    set_error("null descriptor");
+    return PPMLR_INVALID_SPEC;
+  }
+  for (int a = 0; a < 3; ++a)
+    if (d->n[a] < 1) {
+      set_error("block dimensions must be positive");
+      return PPMLR_INVALID_SPEC;
+    }
+  if (d->ghost < 4) {
+    set_error("ghost width must be >= 4");
+    return PPMLR_INVALID_SPEC;
+  }
+  int ndev = 0;
+  CK(cudaGetDeviceCount(&ndev));
+  if (d->device < 0 || d->device >= ndev) {
+    set_error("no such CUDA device");
+    return PPMLR_RUNTIME;
+  }
+  CK(cudaSetDevice(d->device));
+  auto* b = new ppmlr_gpu_block();
+  b->device = d->device;
+  b->g_ref = d->ghost;
+  for (int a = 0; a < 3; ++a) {
+    b->n[a] = d->n[a];
+    b->lo[a] = d->lo[a];
+    b->S[a] = d->n[a] + 2 * kG;
+    b->physical[a][0] = d->physical[a][0];
+    b->physical[a][1] = d->physical[a][1];
+  }
+  b->P0 = ((b->S[0] + 7) / 8) * 8;
+  b->sy = b->P0;
+  b->sz = (long long)b->P0 * b->S[1];
+  b->ncell = b->sz * b->S[2];
+  b->c.gamma = d->gamma;
+  b->c.mu0 = d->mu0;
+  b->c.pressure_floor = d->pressure_floor;
+  b->c.gm1 = d->gamma - 1.0;
+  b->c.two_mu0 = 2.0 * d->mu0;
+  b->boundary = d->boundary;
+  b->wind[0] = d->wind_rho;
+  b->wind[1] = d->wind_v[0];
+  b->wind[2] = d->wind_v[1];
+  b->wind[3] = d->wind_v[2];
+  b->wind[4] = d->wind_imf[0];
+  b->wind[5] = d->wind_imf[1];
+  b->wind[6] = d->wind_imf[2];
+  b->wind[7] = d->wind_p;
+  b->with_dipole = d->with_dipole != 0;
+  b->precision = d->precision;
+  if (d->boundary == PPMLR_BC_PERIODIC)
+    for (int a = 0; a < 3; ++a)
+      if (b->physical[a][0] != b->physical[a][1] || (b->physical[a][0] && b->n[a] < d->ghost)) {
+        b->deferred_error = "periodic boundaries need whole-axis blocks";
+        b->deferred_code = PPMLR_INVALID_SPEC;
+      }
+  auto fail = [&](int rc) {
+    ppmlr_gpu_block_destroy(b);
+    return rc;
+  };
+  int rc = 0;
+  // geometry windows and tables
+  for (int a = 0; a < 3; ++a) {
+    const int off = d->ghost - kG;
+    const int span = b->S[a];
+    b->h_centers[a].assign(d->centers[a] + off, d->centers[a] + off + span);
+    b->h_spacings[a].assign(d->spacings[a] + off, d->spacings[a] + off + span);
+    std::vector<double> slope, qfc, hm, hp;
+    build_axis_tables(b->h_spacings[a], b->h_centers[a], slope, qfc, hm, hp);
+    b->ax[a].span = span;
+    if ((rc = upload_vec(&b->ax[a].dx, b->h_spacings[a]))) return fail(rc);
+    if ((rc = upload_vec(&b->ax[a].slope, slope))) return fail(rc);
+    if ((rc = upload_vec(&b->ax[a].qfc, qfc))) return fail(rc);
+    if ((rc = upload_vec(&b->ax[a].hm, hm))) return fail(rc);
+    if ((rc = upload_vec(&b->ax[a].hp, hp))) return fail(rc);
+  }
+  cudaError_t e;
+  for (int k = 0; k < 2; ++k) {
+    if ((e = cudaMalloc(&b->buf[k], sizeof(double) * 8 * b->ncell)) != cudaSuccess)
+      return fail(cuda_fail(e, "cudaMalloc(state)"));
+    if ((e = cudaMemset(b->buf[k], 0, sizeof(double) * 8 * b->ncell)) != cudaSuccess)
+      return fail(cuda_fail(e, "cudaMemset(state)"));
+  }
+  if (b->with_dipole) {
+    if ((e = cudaMalloc(&b->bd, sizeof(double) * 3 * b->ncell)) != cudaSuccess)
+      return fail(cuda_fail(e, "cudaMalloc(bd)"));
+    cudaMemset(b->bd, 0, sizeof(double) * 3 * b->ncell);
+  }
+  if ((e = cudaMalloc(&b->d_err, 64)) != cudaSuccess) return fail(cuda_fail(e, "cudaMalloc"));
+  b->d_step = b->d_err + 1;
+  b->d_min = b->d_err + 2;
+  b->d_dt = reinterpret_cast<double*>(b->d_err + 3);
+  b->d_dt_prev = reinterpret_cast<double*>(b->d_err + 4);
+  b->d_time = reinterpret_cast<double*>(b->d_err + 5);
+  {
+    unsigned long long init[8] = {kNoError, 0, kInfBits, 0, 0, 0, 0, 0};
+    cudaMemcpy(b->d_err, init, sizeof init, cudaMemcpyHostToDevice);
+  }
+  if ((e = cudaMallocHost(&b->h_pinned, 8 * sizeof(double))) != cudaSuccess)
+    return fail(cuda_fail(e, "cudaMallocHost"));
+  if ((e = cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking)) != cudaSuccess)
+    return fail(cuda_fail(e, "cudaStreamCreate"));
+  choose_sweep_tiles(b);
+  *out = b;
+  return 0;
+}
+
+void ppmlr_gpu_block_destroy(ppmlr_gpu_block* b) {
+  if (!b) return;
+  cudaSetDevice(b->device);
+  if (b->stream) cudaStreamSynchronize(b->stream);
+  for (auto& row : b->graphs)
+    for (auto& g : row)
+      if (g.exec) cudaGraphExecDestroy(g.exec);
+  for (int k = 0; k < 2; ++k) cudaFree(b->buf[k]);
+  cudaFree(b->bd);
+  for (int a = 0; a < 3; ++a) {
+    cudaFree(b->ax[a].dx);
+    cudaFree(b->ax[a].slope);
+    cudaFree(b->ax[a].qfc);
+    cudaFree(b->ax[a].hm);
+    cudaFree(b->ax[a].hp);
+  }
+  cudaFree(b->fslot);
+  cudaFree(b->fstates);
+  cudaFree(b->fidx);
+  cudaFree(b->d_err);
+  cudaFree(b->d_scratch);
+  if (b->h_pinned) cudaFreeHost(b->h_pinned);
+  for (auto& ev : b->ev)
+    if (ev) cudaEventDestroy(ev);
+  for (auto ev : b->timing.pool) cudaEventDestroy(ev);
+  if (b->stream && b->own_stream) cudaStreamDestroy(b->stream);
+  delete b;
+}
+
+static int ensure_scratch(ppmlr_gpu_block* b, size_t bytes) {
+  if (b->scratch_bytes >= bytes) return 0;
+  cudaFree(b->d_scratch);
+  b->d_scratch = nullptr;
+  CK(cudaMalloc(&b->d_scratch, bytes));
+  b->scratch_bytes = bytes;
+  return 0;
+}
+
+int ppmlr_gpu_block_upload(ppmlr_gpu_block* b, const double* fields, const double* bd,
+                           const int64_t* frozen_idx, const double* frozen_states,
+                           int64_t n_frozen) {
+  CK(cudaSetDevice(b->device));
+  CK(cudaStreamSynchronize(b->stream));
+  const int gr = b->g_ref;
+  const int S0r = b->n[0] + 2 * gr, S1r = b->n[1] + 2 * gr, S2r = b->n[2] + 2 * gr;
+  const size_t plane = (size_t)S0r * S1r;
+  const int kchunk = (int)std::max<size_t>(1, std::min<size_t>(S2r, (64ull << 20) / (plane * 64)));
+  if (int rc = ensure_scratch(b, plane * kchunk * 8 * sizeof(double))) return rc;
+  const Lay L = lay_of(b);
+  for (int which = 0; which < 2; ++which) {
+    const double* src = which == 0 ? fields : bd;
+    if (!src) continue;
+    if (which == 1 && !b->with_dipole) continue;
+    const int nper = which == 0 ? 8 : 3;
+    for (int kr0 = 0; kr0 < S2r; kr0 += kchunk) {
+      const int nk = std::min(kchunk, S2r - kr0);
+      CK(cudaMemcpyAsync(b->d_scratch, src + plane * kr0 * nper, plane * nk * nper * 8,
+                         cudaMemcpyHostToDevice, b->stream));
+      for (int k = 0; k < 2; ++k) {
+        if (which == 1 && k == 1) break;
+        aos_to_soa_kernel<<<grid_for(plane * nk), 256, 0, b->stream>>>(
+            which == 0 ? b->d_scratch : nullptr, nper, planes(b->buf[k], b->ncell), L, gr, S0r,
+            S1r, kr0, nk, which == 1 ? b->d_scratch : nullptr, b->bd, b->bd + b->ncell,
+            b->bd + 2 * b->ncell);
+      }
+      CK(cudaGetLastError());
+      CK(cudaStreamSynchronize(b->stream));
+    }
+  }
+  // frozen core: bounding box slot map + SoA states
+  cudaFree(b->fslot);
+  cudaFree(b->fstates);
+  cudaFree(b->fidx);
+  b->fslot = nullptr;
+  b->fstates = nullptr;
+  b->fidx = nullptr;
+  b->n_frozen = n_frozen;
+  if (n_frozen > 0) {
+    int lo[3] = {1 << 30, 1 << 30, 1 << 30}, hi[3] = {-1, -1, -1};
+    std::vector<int> ijk(3 * n_frozen);
+    std::vector<long long> didx(n_frozen);
+    for (int64_t f = 0; f < n_frozen; ++f) {
+      const int64_t r = frozen_idx[f];
+      const int i = (int)(r % S0r) - gr, j = (int)((r / S0r) % S1r) - gr,
+                k = (int)(r / ((int64_t)S0r * S1r)) - gr;
+      if (i < 0 || j < 0 || k < 0 || i >= b->n[0] || j >= b->n[1] || k >= b->n[2]) {
+        set_error("frozen-core index outside the block interior");
+        return PPMLR_INVALID_SPEC;
+      }
+      ijk[3 * f] = i;
+      ijk[3 * f + 1] = j;
+      ijk[3 * f + 2] = k;
+      const int c3[3] = {i, j, k};
+      for (int a = 0; a < 3; ++a) {
+        lo[a] = std::min(lo[a], c3[a]);
+        hi[a] = std::max(hi[a], c3[a]);
+      }
+      didx[f] = L.idx(i, j, k);
+    }
+    for (int a = 0; a < 3; ++a) {
+      b->fbox_lo[a] = lo[a];
+      b->fbox_n[a] = hi[a] - lo[a] + 1;
+    }
+    const size_t vol = (size_t)b->fbox_n[0] * b->fbox_n[1] * b->fbox_n[2];
+    std::vector<int> slot(vol, -1);
+    std::vector<double> st(8 * (size_t)n_frozen);
+    for (int64_t f = 0; f < n_frozen; ++f) {
+      const size_t v = (size_t)(ijk[3 * f] - lo[0]) +
+                       b->fbox_n[0] * ((size_t)(ijk[3 * f + 1] - lo[1]) +
+                                       b->fbox_n[1] * (size_t)(ijk[3 * f + 2] - lo[2]));
+      slot[v] = (int)f;  // later entries win, like sequential restore
+      for (int q = 0; q < 8; ++q) st[(size_t)q * n_frozen + f] = frozen_states[8 * f + q];
+    }
+    if (int rc = upload_vec(&b->fslot, slot)) return rc;
+    if (int rc = upload_vec(&b->fstates, st)) return rc;
+    if (int rc = upload_vec(&b->fidx, didx)) return rc;
+  }
+  // Magnetosphere: constant sunward shell in both buffers.
+  if (b->boundary == PPMLR_BC_MAGNETOSPHERE && b->physical[0][1]) {
+    for (int k = 0; k < 2; ++k)
+      wind_fill_kernel<<<grid_for((long long)kG * b->n[1] * b->n[2]), 256, 0, b->stream>>>(
+          planes(b->buf[k], b->ncell), L, b->bd, b->bd ? b->bd + b->ncell : nullptr,
+          b->bd ? b->bd + 2 * b->ncell : nullptr, b->wind[0], b->wind[7], b->wind[1],
+          b->wind[2], b->wind[3], b->wind[4], b->wind[5], b->wind[6]);
+    CK(cudaGetLastError());
+  }
+  b->cur = 0;
+  {
+    unsigned long long init[6] = {kNoError, 0, kInfBits, 0, 0, 0};
+    CK(cudaMemcpyAsync(b->d_err, init, sizeof init, cudaMemcpyHostToDevice, b->stream));
+  }
+  b->step_base = 0;
+  CK(cudaStreamSynchronize(b->stream));
+  return 0;
+}
+
+static int download_impl(ppmlr_gpu_block* b, double* fields, bool interior_only) {
+  CK(cudaSetDevice(b->device));
+  const Lay L = lay_of(b);
+  if (interior_only) {
+    const size_t cells = (size_t)b->n[0] * b->n[1] * b->n[2];
+    if (int rc = ensure_scratch(b, cells * 64)) return rc;
+    soa_to_interior_kernel<<<grid_for(cells), 256, 0, b->stream>>>(
+        b->d_scratch, planes(cur_buf(b), b->ncell), L);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(fields, b->d_scratch, cells * 64, cudaMemcpyDeviceToHost, b->stream));
+    CK(cudaStreamSynchronize(b->stream));
+    return 0;
+  }
+  const int gr = b->g_ref;
+  const int S0r = b->n[0] + 2 * gr, S1r = b->n[1] + 2 * gr, S2r = b->n[2] + 2 * gr;
+  const size_t plane = (size_t)S0r * S1r;
+  const int kchunk = (int)std::max<size_t>(1, std::min<size_t>(S2r, (64ull << 20) / (plane * 64)));
+  if (int rc = ensure_scratch(b, plane * kchunk * 64)) return rc;
+  for (int kr0 = 0; kr0 < S2r; kr0 += kchunk) {
+    const int nk = std::min(kchunk, S2r - kr0);
+    soa_to_aos_kernel<<<grid_for(plane * nk), 256, 0, b->stream>>>(
+        b->d_scratch, planes(cur_buf(b), b->ncell), L, gr, S0r, S1r, kr0, nk);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(fields + plane * kr0 * 8, b->d_scratch, plane * nk * 64,
+                       cudaMemcpyDeviceToHost, b->stream));
+    CK(cudaStreamSynchronize(b->stream));
+  }
+  return 0;
+}
+
+int ppmlr_gpu_block_download(ppmlr_gpu_block* b, double* fields) {
+  return download_impl(b, fields, false);
+}
+int ppmlr_gpu_block_download_interior(ppmlr_gpu_block* b, double* out) {
+  return download_impl(b, out, true);
+}
+
+int ppmlr_gpu_block_check(ppmlr_gpu_block* b) {
+  CK(cudaSetDevice(b->device));
+  CK(cudaMemcpyAsync(b->h_pinned, b->d_err, 8, cudaMemcpyDeviceToHost, b->stream));
+  CK(cudaStreamSynchronize(b->stream));
+  unsigned long long key;
+  std::memcpy(&key, b->h_pinned, 8);
+  if (key == kNoError) return 0;
+  std::string msg;
+  const int rc = decode_error(b, key, msg);
+  set_error(msg);
+  const unsigned long long reset = kNoError;
+  cudaMemcpy(b->d_err, &reset, 8, cudaMemcpyHostToDevice);
+  return rc;
+}
+
+static int deferred(ppmlr_gpu_block* b) {
+  if (b->deferred_code) {
+    set_error(b->deferred_error);
+    return b->deferred_code;
+  }
+  return 0;
+}
+
+int ppmlr_gpu_block_compute_dt(ppmlr_gpu_block* b, double cfl, double* dt_out) {
+  CK(cudaSetDevice(b->device));
+  if (int rc = launch_cfl(b, 0)) return rc;
+  if (int rc = launch_step_end(b, cfl, 0, 1)) return rc;
+  CK(cudaMemcpyAsync(b->h_pinned, b->d_dt, 8, cudaMemcpyDeviceToHost, b->stream));
+  if (int rc = ppmlr_gpu_block_check(b)) return rc;
+  *dt_out = b->h_pinned[0];
+  return 0;
+}
+
+int ppmlr_gpu_block_local_dt_async(ppmlr_gpu_block* b, double cfl) {
+  CK(cudaSetDevice(b->device));
+  if (int rc = launch_cfl(b, 0)) return rc;
+  return launch_step_end(b, cfl, 0, 1);
+}
+
+double* ppmlr_gpu_block_dt_slot(ppmlr_gpu_block* b) { return b->d_dt; }
+
+
+int ppmlr_gpu_block_fill_boundaries(ppmlr_gpu_block* b, int axis_mask, int layers) {
+  if (int rc = deferred(b)) return rc;
+  CK(cudaSetDevice(b->device));
+  if (layers < 1 || layers > kG) {
+    set_error("fill_boundaries: layers must be in 1..4");
+    return PPMLR_INVALID_SPEC;
+  }
+  return launch_bc(b, axis_mask, layers);
+}
+
+int ppmlr_gpu_block_sweep(ppmlr_gpu_block* b, int axis, double dt) {
+  CK(cudaSetDevice(b->device));
+  if (axis < 0 || axis > 2) {
+    set_error("sweep: axis must be 0, 1 or 2");
+    return PPMLR_INVALID_SPEC;
+  }
+  if (int rc = block_set_dt(b, dt)) return rc;
+  // The sweep writes only interior cells of the other buffer; carry the
+  // untouched cells (ghosts) over so the block behaves in place.
+  CK(cudaMemcpyAsync(b->buf[b->cur ^ 1], b->buf[b->cur], sizeof(double) * 8 * b->ncell,
+                     cudaMemcpyDeviceToDevice, b->stream));
+  if (int rc = launch_sweep(b, axis, kPhaseSweep0 + axis)) return rc;
+  return 0;
+}
+
+int ppmlr_gpu_block_sources(ppmlr_gpu_block* b, double dt) {
+  CK(cudaSetDevice(b->device));
+  if (int rc = block_set_dt(b, dt)) return rc;
+  CK(cudaMemcpyAsync(b->buf[b->cur ^ 1], b->buf[b->cur], sizeof(double) * 8 * b->ncell,
+                     cudaMemcpyDeviceToDevice, b->stream));
+  // standalone apply_sources: no frozen override, no fused CFL
+  const long long nf = b->n_frozen;
+  b->n_frozen = 0;
+  const int rc = launch_sources(b, 0);
+  b->n_frozen = nf;
+  return rc;
+}
+
+int ppmlr_gpu_block_restore_frozen(ppmlr_gpu_block* b) {
+  CK(cudaSetDevice(b->device));
+  return launch_frozen(b);
+}
+
+// One full step of a whole-domain block, stream-ordered, dt already in d_dt.
+static int enqueue_step(ppmlr_gpu_block* b, double cfl, int with_sources, int parity) {
+  static const int order[2][3] = {{0, 1, 2}, {2, 1, 0}};
+  for (int s = 0; s < 3; ++s) {
+    const int axis = order[parity][s];
+    if (int rc = launch_bc(b, 1 << axis, kG)) return rc;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (b->timing.enabled) {
+      auto& t = b->timing;
+      while (t.pool.size() < t.used + 2) {
+        cudaEvent_t e;
+        CK(cudaEventCreate(&e));
+        t.pool.push_back(e);
+      }
+      e0 = t.pool[t.used];
+      e1 = t.pool[t.used + 1];
+      t.used += 2;
+      CK(cudaEventRecord(e0, b->stream));
+    }
+    if (int rc = launch_sweep(b, axis, kPhaseSweep0 + s)) return rc;
+    if (e1) CK(cudaEventRecord(e1, b->stream));
+  }
+  if (with_sources) {
+    if (int rc = launch_bc(b, 7, 1)) return rc;
+    if (int rc = launch_sources(b, 1)) return rc;
+  } else {
+    if (int rc = launch_frozen(b)) return rc;
+    if (int rc = launch_cfl(b, 1)) return rc;
+  }
+  return launch_step_end(b, cfl, 1, 1);
+}
+
+static int run_steps(ppmlr_gpu_block* b, double cfl, int with_sources, long first_step,
+                     long steps) {
+  if (int rc = deferred(b)) return rc;
+  CK(cudaSetDevice(b->device));
+  // fresh error window; keys count steps from first_step
+  {
+    unsigned long long init[2] = {kNoError, 0};
+    CK(cudaMemcpyAsync(b->d_err, init, sizeof init, cudaMemcpyHostToDevice, b->stream));
+    b->step_base = first_step;
+  }
+  // dt of the first step
+  if (int rc = launch_cfl(b, 0)) return rc;
+  if (int rc = launch_step_end(b, cfl, 0, 1)) return rc;
+  const bool use_graph = !b->timing.enabled && env_int("PPMLR_NO_GRAPH", 0) == 0;
+  for (long s = 0; s < steps; ++s) {
+    const int parity = (first_step + s) % 2 == 0 ? 0 : 1;
+    if (!use_graph) {
+      if (int rc = enqueue_step(b, cfl, with_sources, parity)) return rc;
+      continue;
+    }
+    StepGraph& g = b->graphs[parity][b->cur];
+    const int cur0 = b->cur;
+    if (!g.exec || g.with_sources != with_sources || g.cfl != cfl) {
+      if (g.exec) cudaGraphExecDestroy(g.exec);
+      g.exec = nullptr;
+      cudaGraph_t graph;
+      CK(cudaStreamBeginCapture(b->stream, cudaStreamCaptureModeThreadLocal));
+      const int rc = enqueue_step(b, cfl, with_sources, parity);
+      cudaError_t e = cudaStreamEndCapture(b->stream, &graph);
+      if (rc) return rc;
+      if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture");
+      CK(cudaGraphInstantiate(&g.exec, graph, 0));
+      cudaGraphDestroy(graph);
+      g.with_sources = with_sources;
+      g.parity = parity;
+      g.cfl = cfl;
+      g.cur = b->cur;  // buffer after the step
+      b->cur = cur0;
+    }
+    CK(cudaGraphLaunch(g.exec, b->stream));
+    b->cur = g.cur;
+  }
+  return 0;
+}
+
+int ppmlr_gpu_block_advance(ppmlr_gpu_block* b, double cfl, int with_sources, long step,
+                            double* dt_out) {
+  if (int rc = run_steps(b, cfl, with_sources, step, 1)) return rc;
+  CK(cudaMemcpyAsync(b->h_pinned + 2, b->d_dt_prev, 8, cudaMemcpyDeviceToHost, b->stream));
+  if (int rc = ppmlr_gpu_block_check(b)) return rc;
+  if (dt_out) *dt_out = b->h_pinned[2];
+  return 0;
+}
+
+int ppmlr_gpu_block_run(ppmlr_gpu_block* b, double cfl, int with_sources, long first_step,
+                        long steps, double* time_out) {
+  if (steps <= 0) return 0;
+  if (time_out) {
+    b->h_pinned[3] = *time_out;
+    CK(cudaMemcpyAsync(b->d_time, &b->h_pinned[3], 8, cudaMemcpyHostToDevice, b->stream));
+  }
+  if (int rc = run_steps(b, cfl, with_sources, first_step, steps)) return rc;
+  CK(cudaMemcpyAsync(b->h_pinned + 4, b->d_time, 8, cudaMemcpyDeviceToHost, b->stream));
+  if (int rc = ppmlr_gpu_block_check(b)) return rc;
+  if (time_out) *time_out = b->h_pinned[4];
+  return 0;
+}
+
+int ppmlr_gpu_block_pack_face(ppmlr_gpu_block* b, int face, int layers, double* dev_buf) {
+  CK(cudaSetDevice(b->device));
+  if (face < 0 || face > 5 || layers < 1 || layers > kG) {
+    set_error("pack_face: bad face or layer count");
+    return PPMLR_INVALID_SPEC;
+  }
+  const int axis = face / 2;
+  const long long work = (long long)layers * b->n[(axis + 1) % 3] * b->n[(axis + 2) % 3];
+  pack_kernel<<<grid_for(work), 256, 0, b->stream>>>(planes(cur_buf(b), b->ncell), lay_of(b),
+                                                       face, layers, dev_buf);
+  CK(cudaGetLastError());
+  return 0;
+}
+
+int ppmlr_gpu_block_unpack_face(ppmlr_gpu_block* b, int face, int layers,
+                                const double* dev_buf) {
+  CK(cudaSetDevice(b->device));
+  if (face < 0 || face > 5 || layers < 1 || layers > kG) {
+    set_error("unpack_face: bad face or layer count");
+    return PPMLR_INVALID_SPEC;
+  }
+  const int axis = face / 2;
+  const long long work = (long long)layers * b->n[(axis + 1) % 3] * b->n[(axis + 2) % 3];
+  unpack_kernel<<<grid_for(work), 256, 0, b->stream>>>(planes(cur_buf(b), b->ncell),
+                                                         lay_of(b), face, layers, dev_buf);
+  CK(cudaGetLastError());
+  return 0;
+}
+
+int ppmlr_gpu_block_copy_face(ppmlr_gpu_block* dst, int face, ppmlr_gpu_block* src,
+                              int layers) {
+  CK(cudaSetDevice(dst->device));
+  const int axis = face / 2;
+  if (dst->n[(axis + 1) % 3] != src->n[(axis + 1) % 3] ||
+      dst->n[(axis + 2) % 3] != src->n[(axis + 2) % 3]) {
+    set_error("halo slab face span does not match block face");
+    return PPMLR_INVALID_SPEC;
+  }
+  const long long work = (long long)layers * dst->n[(axis + 1) % 3] * dst->n[(axis + 2) % 3];
+  copy_face_kernel<<<grid_for(work), 256, 0, dst->stream>>>(
+      planes(cur_buf(dst), dst->ncell), lay_of(dst), planes(cur_buf(src), src->ncell),
+      lay_of(src), face, layers);
+  CK(cudaGetLastError());
+  return 0;
+}
+
+void* ppmlr_gpu_block_stream(ppmlr_gpu_block* b) { return b->stream; }
+
+int ppmlr_gpu_block_set_stream(ppmlr_gpu_block* b, void* stream) {
+  CK(cudaSetDevice(b->device));
+  CK(cudaStreamSynchronize(b->stream));
+  if (b->own_stream) cudaStreamDestroy(b->stream);
+  b->stream = static_cast<cudaStream_t>(stream);
+  b->own_stream = false;
+  for (auto& row : b->graphs)
+    for (auto& g : row)
+      if (g.exec) {
+        cudaGraphExecDestroy(g.exec);
+        g.exec = nullptr;
+      }
+  return 0;
+}
+
+int ppmlr_gpu_block_synchronize(ppmlr_gpu_block* b) {
+  CK(cudaSetDevice(b->device));
+  CK(cudaStreamSynchronize(b->stream));
+  return 0;
+}
+
+int ppmlr_gpu_block_timing(ppmlr_gpu_block* b, int enable, double* sweep_ms, double* total_ms,
+                           long* launches) {
+  CK(cudaSetDevice(b->device));
+  auto& t = b->timing;
+  CK(cudaStreamSynchronize(b->stream));
+  double sum = 0.0;
+  for (size_t i = 0; i + 1 < t.used; i += 2) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, t.pool[i], t.pool[i + 1]));
+    sum += ms;
+  }
+  if (sweep_ms) *sweep_ms = sum;
+  if (launches) *launches = (long)(t.used / 2);
+  if (total_ms) *total_ms = (double)b->kernel_launches;  // kernel launch count since reset
+  t.used = 0;
+  b->kernel_launches = 0;
+  t.enabled = enable != 0;
+  return 0;
+}
+
+int ppmlr_gpu_sweep_strips(double* states, const double* bd, const double* dx, int n,
+                           int ghost, int nstrips, int dir, double dt, double gamma,
+                           double mu0, double pressure_floor, int precision, int device) {
+  if (n < 1 || nstrips < 1 || ghost < 4 || dir < 0 || dir > 2) {
+    set_error("sweep_strips: bad arguments");
+    return PPMLR_INVALID_SPEC;
+  }
+  // A block whose `dir` axis is the strip and whose (dir+1) axis enumerates
+  // the strips; ghost cells are the caller's (no boundary fill).
+  const int nn = n + 2 * ghost;
+  std::vector<double> zero_c(std::max(nstrips, 1) + 2 * ghost, 0.0),
+      one_s(std::max(nstrips, 1) + 2 * ghost, 1.0), cen(nn);
+  for (int i = 0; i < nn; ++i) cen[i] = i;
+  ppmlr_gpu_block_desc d{};
+  const int t1 = (dir + 1) % 3, t2 = (dir + 2) % 3;
+  d.n[dir] = n;
+  d.n[t1] = nstrips;
+  d.n[t2] = 1;
+  d.ghost = ghost;
+  std::vector<double> c1(nstrips + 2 * ghost), s1(nstrips + 2 * ghost, 1.0), c2(1 + 2 * ghost),
+      s2(1 + 2 * ghost, 1.0);
+  d.centers[dir] = cen.data();
+  d.spacings[dir] = dx;
+  d.centers[t1] = c1.data();
+  d.spacings[t1] = s1.data();
+  d.centers[t2] = c2.data();
+  d.spacings[t2] = s2.data();
+  d.gamma = gamma;
+  d.mu0 = mu0;
+  d.pressure_floor = pressure_floor;
+  d.with_dipole = bd != nullptr;
+  d.precision = precision;
+  d.device = device;
+  ppmlr_gpu_block* b = nullptr;
+  if (int rc = ppmlr_gpu_block_create(&d, &b)) return rc;
+  // Scatter strips into a ghost-inclusive reference-layout array.
+  const int S0 = d.n[0] + 2 * ghost, S1 = d.n[1] + 2 * ghost, S2 = d.n[2] + 2 * ghost;
+  std::vector<double> f((size_t)S0 * S1 * S2 * 8, 1.0), bdv;
+  if (bd) bdv.assign((size_t)S0 * S1 * S2 * 3, 0.0);
+  auto lin = [&](int q, int s) {
+    int c[3];
+    c[dir] = q;            // 0..nn-1 (ghost-inclusive)
+    c[t1] = s + ghost;
+    c[t2] = ghost;
+    return (size_t)c[0] + (size_t)S0 * (c[1] + (size_t)S1 * c[2]);
+  };
+  for (int s = 0; s < nstrips; ++s)
+    for (int q = 0; q < nn; ++q) {
+      const size_t l = lin(q, s);
+      std::memcpy(&f[8 * l], states + ((size_t)s * nn + q) * 8, 64);
+      if (bd) std::memcpy(&bdv[3 * l], bd + ((size_t)s * nn + q) * 3, 24);
+    }
+  int rc = ppmlr_gpu_block_upload(b, f.data(), bd ? bdv.data() : nullptr, nullptr, nullptr, 0);
+  if (!rc) {
+    b->step_base = 0;
+    rc = ppmlr_gpu_block_sweep(b, dir, dt);
+  }
+  if (!rc) {
+    // error keys of a bare sweep: phase Sweep0 + dir maps back to `dir`
+    unsigned long long key = 0;
+    cudaMemcpy(&key, b->d_err, 8, cudaMemcpyDeviceToHost);
+    if (key != kNoError) {
+      std::string msg;
+      rc = decode_error(b, key, msg);
+      // strip-level message: drop the " in sweep axis" suffix and report the
+      // sweep_1d exception kind (StepRejected vs UnphysicalState)
+      const size_t cut = msg.find(" in sweep axis");
+      const std::string inner = cut == std::string::npos ? msg : msg.substr(0, cut);
+      set_error(inner);
+      rc = inner.rfind("Lagrangian interfaces crossed", 0) == 0 ? PPMLR_STEP_REJECTED
+                                                                  : PPMLR_UNPHYSICAL;
+      // report the first failing strip (pencil order = strip index)
+    }
+  }
+  if (!rc) rc = ppmlr_gpu_block_download(b, f.data());
+  if (!rc)
+    for (int s = 0; s < nstrips; ++s)
+      for (int q = ghost; q < ghost + n; ++q)
+        std::memcpy(states + ((size_t)s * nn + q) * 8, &f[8 * lin(q, s)], 64);
+  ppmlr_gpu_block_destroy(b);
+  return rc;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------
+// FP64 pipe peak: independent DFMA chains (MEASURED_PEAKS.json carries no
+// FP64 figure; SURVEY.md §8(d) asks for a measured denominator).
+namespace {
+__global__ void dfma_peak_kernel(double* out, int iters, double a, double b) {
+  double x[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) x[k] = threadIdx.x * 1e-9 + k;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = fma(x[k], a, b);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += x[k];
+  if (s == 12345.678) out[0] = s;  // keep the chains live
+}
+}  // namespace
+
+extern "C" int ppmlr_gpu_fp64_peak(int device, double* tflops) {
+  CK(cudaSetDevice(device));
+  int sms = 0;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  double* d = nullptr;
+  CK(cudaMalloc(&d, 8));
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int iters = 20000, threads = 512, blocks = sms * 4;
+  dfma_peak_kernel<<<blocks, threads>>>(d, 1000, 0.999999, 1e-7);  // warm-up
+  float best = 1e30f;
+  for (int rep = 0; rep < 5; ++rep) {
+    cudaEventRecord(e0);
+    dfma_peak_kernel<<<blocks, threads>>>(d, iters, 0.999999, 1e-7);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    best = ms < best ? ms : best;
+  }
+  const cudaError_t err = cudaGetLastError();
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(d);
+  if (err != cudaSuccess) return cuda_fail(err, "dfma_peak_kernel");
+  const double flops = 2.0 * 8.0 * (double)iters * threads * blocks;
+  *tflops = flops / (best * 1e-3) / 1e12;
+  return 0;
+}

@@ -1,0 +1,113 @@
+// Internal definition of a device-resident block (BlockState on one B200).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/ppmlr_gpu.h"
+#include "ppmlr_dev.cuh"
+
+namespace ppmlr_b200 {
+
+constexpr int kG = 4;  // device ghost width (the dependency window)
+
+// Per-axis device geometry, ghost-inclusive with kG ghosts (span = n + 8).
+struct DevAxis {
+  double* dx = nullptr;     // spacings
+  double* slope = nullptr;  // 3 per position: limited_slope coefficients
+  double* qfc = nullptr;    // 5 per edge: interface-value coefficients
+  double* hm = nullptr;     // centers[l] - centers[l-1]   (apply_sources)
+  double* hp = nullptr;     // centers[l+1] - centers[l]
+  int span = 0;
+};
+
+struct SweepTiming {
+  bool enabled = false;
+  std::vector<cudaEvent_t> pool;  // pairs (start, end) per sweep launch
+  size_t used = 0;                // events consumed in the pool
+  double sweep_ms = 0.0, total_ms = 0.0;
+  long launches = 0;              // sweep launches timed
+};
+
+struct StepGraph {
+  cudaGraphExec_t exec = nullptr;
+  int parity = -1;
+  int with_sources = -1;
+  int cur = -1;
+  double cfl = -1.0;
+};
+
+}  // namespace ppmlr_b200
+
+struct ppmlr_gpu_block {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = true;
+  int n[3] = {0, 0, 0};
+  int lo[3] = {0, 0, 0};
+  int g_ref = 4;             // ghost width of the caller's arrays
+  int S[3] = {0, 0, 0};      // n + 8
+  int P0 = 0;                // padded x pitch (>= S[0], multiple of 8)
+  long long sx = 1, sy = 0, sz = 0;
+  long long ncell = 0;       // elements per field plane
+  double* buf[2] = {nullptr, nullptr};  // 8 planes each
+  int cur = 0;               // buffer holding the current state
+  double* bd = nullptr;      // 3 planes or nullptr
+  ppmlr_b200::DevAxis ax[3];
+  std::vector<double> h_centers[3], h_spacings[3];  // kG-ghost windows
+  int physical[3][2] = {{0, 0}, {0, 0}, {0, 0}};
+  ppmlr_b200::Consts c{};
+  int boundary = 0;
+  double wind[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  bool with_dipole = false;
+  int precision = PPMLR_STRICT;
+  std::string deferred_error;  // e.g. periodic on a partial axis (apply_boundaries)
+  int deferred_code = 0;
+  // frozen inner core: bounding box + slot map
+  long long n_frozen = 0;
+  int fbox_lo[3] = {0, 0, 0}, fbox_n[3] = {0, 0, 0};
+  int* fslot = nullptr;        // fbox volume, -1 = not frozen
+  double* fstates = nullptr;   // 8 planes of n_frozen
+  long long* fidx = nullptr;   // device linear indices (for the standalone restore)
+  // device scalars
+  unsigned long long* d_err = nullptr;   // first-failure key
+  unsigned long long* d_step = nullptr;  // step counter for keys (relative)
+  unsigned long long* d_min = nullptr;   // CFL min as ordered bits
+  double* d_dt = nullptr;                // dt in use
+  double* d_dt_prev = nullptr;           // dt of the last completed step
+  double* d_time = nullptr;              // accumulated time
+  double* h_pinned = nullptr;            // 8 doubles pinned scratch
+  long step_base = 0;                    // absolute step of d_step == 0
+  double* d_scratch = nullptr;           // staging for upload/download
+  size_t scratch_bytes = 0;
+  ppmlr_b200::StepGraph graphs[2][2];    // [parity][cur]
+  ppmlr_b200::SweepTiming timing;
+  cudaEvent_t ev[8] = {};
+  long kernel_launches = 0;              // every kernel this block enqueued
+  int sweep_L[3] = {0, 0, 0};            // segment length per axis
+  int sweep_threads[3] = {0, 0, 0};
+};
+
+namespace ppmlr_b200 {
+void set_error(const std::string& msg);
+int cuda_fail(cudaError_t e, const char* where);
+// Launchers implemented in sweep_*.cu
+struct SweepArgs;
+cudaError_t launch_sweep_strict(int axis, bool dipole, const SweepArgs& a, int threads,
+                                size_t smem, cudaStream_t st);
+cudaError_t launch_sweep_fast(int axis, bool dipole, const SweepArgs& a, int threads,
+                              size_t smem, cudaStream_t st);
+}  // namespace ppmlr_b200
+
+namespace ppmlr_b200 {
+// Stream-ordered building blocks of a step (block.cu); used by the harness.
+int launch_sweep(ppmlr_gpu_block* b, int axis, int phase);  // flips b->cur
+int launch_bc(ppmlr_gpu_block* b, int axis_mask, int layers);
+int launch_sources(ppmlr_gpu_block* b, int fuse_cfl);      // flips b->cur
+int launch_frozen(ppmlr_gpu_block* b);
+int launch_cfl(ppmlr_gpu_block* b, unsigned long long step_add);
+int launch_step_end(ppmlr_gpu_block* b, double cfl, int close_step, int have_min);
+int block_set_dt(ppmlr_gpu_block* b, double dt);  // dt < 0: keep the device slot
+}  // namespace ppmlr_b200

@@ -1,0 +1,6 @@
+// Fast sweep: compiled with --fmad=true and PPMLR_FAST_MATH (reciprocal folding);
+// gated by the tolerance in DESIGN.md / tests/test_gpu_parity.py.
+#define PPMLR_FAST_MATH 1
+#define PPMLR_KNS fast
+#define PPMLR_LAUNCH_NAME launch_sweep_fast
+#include "sweep_launch.inc"
