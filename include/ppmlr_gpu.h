@@ -155,6 +155,21 @@ int ppmlr_gpu_block_unpack_face(ppmlr_gpu_block* b, int face, int layers,
  * `layers` outermost interior layers of src's opposite face. */
 int ppmlr_gpu_block_copy_face(ppmlr_gpu_block* dst, int face, ppmlr_gpu_block* src,
                               int layers);
+/* Stream-ordered pieces of Harness::advance for an external (multi-process)
+ * driver that owns the halo exchange and the dt reduction:
+ *   begin:      reset the error window; dt slot <- this block's cfl*min
+ *               (then min-reduce the dt slot across ranks)
+ *   sweep_async: sweep_axis along `axis` as sweep number order_index (0..2)
+ *               of the step, dt from the dt slot; ghosts must be current
+ *   end_step:   apply_sources (+frozen core) or the frozen core alone, close
+ *               the step (time += dt) and put the next local cfl*min in
+ *               the dt slot (min-reduce it again before the next step)
+ * Errors are reported by ppmlr_gpu_block_check(). */
+int ppmlr_gpu_block_begin(ppmlr_gpu_block* b, double cfl, long first_step);
+int ppmlr_gpu_block_sweep_async(ppmlr_gpu_block* b, int axis, int order_index);
+int ppmlr_gpu_block_end_step(ppmlr_gpu_block* b, double cfl, int with_sources);
+/* Simulated time accumulated on the device (host sync). */
+int ppmlr_gpu_block_time(ppmlr_gpu_block* b, double* time_out);
 /* Device scalars for external drivers (e.g. an NCCL min all-reduce of dt):
  * the block's dt slot (double) used by sweeps/sources issued with dt < 0. */
 double* ppmlr_gpu_block_dt_slot(ppmlr_gpu_block* b);

@@ -1303,6 +1303,44 @@ int ppmlr_gpu_block_copy_face(ppmlr_gpu_block* dst, int face, ppmlr_gpu_block* s
   return 0;
 }
 
+int ppmlr_gpu_block_begin(ppmlr_gpu_block* b, double cfl, long first_step) {
+  if (int rc = deferred(b)) return rc;
+  CK(cudaSetDevice(b->device));
+  unsigned long long init[2] = {kNoError, 0};
+  CK(cudaMemcpyAsync(b->d_err, init, sizeof init, cudaMemcpyHostToDevice, b->stream));
+  b->step_base = first_step;
+  if (int rc = launch_cfl(b, 0)) return rc;
+  return launch_step_end(b, cfl, 0, 1);
+}
+
+int ppmlr_gpu_block_sweep_async(ppmlr_gpu_block* b, int axis, int order_index) {
+  CK(cudaSetDevice(b->device));
+  if (axis < 0 || axis > 2 || order_index < 0 || order_index > 2) {
+    set_error("sweep_async: bad axis/order");
+    return PPMLR_INVALID_SPEC;
+  }
+  return launch_sweep(b, axis, kPhaseSweep0 + order_index);
+}
+
+int ppmlr_gpu_block_end_step(ppmlr_gpu_block* b, double cfl, int with_sources) {
+  CK(cudaSetDevice(b->device));
+  if (with_sources) {
+    if (int rc = launch_sources(b, 1)) return rc;
+  } else {
+    if (int rc = launch_frozen(b)) return rc;
+    if (int rc = launch_cfl(b, 1)) return rc;
+  }
+  return launch_step_end(b, cfl, 1, 1);
+}
+
+int ppmlr_gpu_block_time(ppmlr_gpu_block* b, double* time_out) {
+  CK(cudaSetDevice(b->device));
+  CK(cudaMemcpyAsync(b->h_pinned + 5, b->d_time, 8, cudaMemcpyDeviceToHost, b->stream));
+  CK(cudaStreamSynchronize(b->stream));
+  *time_out = b->h_pinned[5];
+  return 0;
+}
+
 void* ppmlr_gpu_block_stream(ppmlr_gpu_block* b) { return b->stream; }
 
 int ppmlr_gpu_block_set_stream(ppmlr_gpu_block* b, void* stream) {

@@ -1,0 +1,277 @@
+"""Multi-GPU driver: one process (rank) per GPU, one block per rank.
+
+The reference's in-process harness (harness.cpp:59-92, exchange.cpp:93-149)
+becomes a distributed step over torch.distributed (NCCL over NVLink on the
+B200 box, gloo for the CPU tests):
+
+  dt       <- all_reduce(MIN) of every rank's cfl*min   (compute_global_dt)
+  for axis in XYZ / ZYX:
+      halo exchange of the `axis` faces, 4 layers        (exchange_step)
+      physical-face fill along `axis`                    (apply_boundaries)
+      sweep                                              (sweep_axis)
+  halo exchange of all faces, 1 layer; fill; sources + frozen core; the
+  next local cfl*min fused into the sources epilogue; all_reduce(MIN)
+
+Only what the next kernel reads is exchanged (ghosts are
+pure copies, so this is bit-identical to the reference's 4-layer,
+all-face exchanges; the ledger keeps the reference's accounting).  Slabs
+are packed in the reference's HaloSlab order.  The kernel work of a rank is
+issued on torch's current stream, so NCCL and the kernels are stream-ordered
+with no host synchronisation inside a step.
+
+The step logic (``advance``) is written against a small block interface so
+the same code runs with the CUDA block (``DeviceRankBlock``) and, in the CPU
+tests, with an oracle-backed block over gloo.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+import os
+import time
+
+import numpy as np
+
+ORDER = ((0, 1, 2), (2, 1, 0))  # sweep_order (stepper.cpp:288-290)
+
+
+class _CudaPtr:
+    """__cuda_array_interface__ view of device memory owned by the library."""
+
+    def __init__(self, ptr, n, typestr="<f8"):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr,
+                                         "data": (int(ptr), False), "version": 3}
+
+
+def face_cells(n, face):
+    a = face // 2
+    return n[(a + 1) % 3] * n[(a + 2) % 3]
+
+
+class Exchanger:
+    """Halo slabs between neighbour ranks with torch.distributed P2P."""
+
+    def __init__(self, info, n, make_buffer, group=None):
+        self.info = info
+        self.n = n
+        self.group = group
+        self.send = {}
+        self.recv = {}
+        for face in range(6):
+            if info.neighbor[face] >= 0:
+                cnt = face_cells(n, face) * 4 * 8
+                self.send[face] = make_buffer(cnt)
+                self.recv[face] = make_buffer(cnt)
+        self.messages = 0
+        self.bytes_moved = 0
+
+    def exchange(self, blk, faces, layers):
+        import torch.distributed as dist
+        faces = [f for f in faces if self.info.neighbor[f] >= 0]
+        if not faces:
+            return
+        ops = []
+        for f in faces:
+            cnt = face_cells(self.n, f) * layers * 8
+            blk.pack_face(f, layers, self.send[f])
+            nb = self.info.neighbor[f]
+            ops.append(dist.P2POp(dist.isend, self.send[f][:cnt], nb, self.group))
+            ops.append(dist.P2POp(dist.irecv, self.recv[f][:cnt], nb, self.group))
+            self.messages += 1
+            self.bytes_moved += cnt * 8
+        for r in dist.batch_isend_irecv(ops):
+            r.wait()
+        for f in faces:
+            blk.unpack_face(f, layers, self.recv[f])
+
+
+def begin(blk, cfl, first_step, group=None):
+    import torch.distributed as dist
+    blk.begin(cfl, first_step)
+    dist.all_reduce(blk.dt_tensor(), op=dist.ReduceOp.MIN, group=group)
+
+
+def advance(blk, ex, step, cfl, with_sources, group=None):
+    """One distributed Harness::advance; the dt slot holds the global dt on
+    entry and the next step's global dt on exit."""
+    import torch.distributed as dist
+    order = ORDER[0 if step % 2 == 0 else 1]
+    for s, axis in enumerate(order):
+        ex.exchange(blk, (2 * axis, 2 * axis + 1), 4)
+        blk.fill_boundaries(1 << axis, 4)
+        blk.sweep_async(axis, s)
+    if with_sources:
+        ex.exchange(blk, range(6), 1)
+        blk.fill_boundaries(7, 1)
+    blk.end_step(cfl, with_sources)
+    dist.all_reduce(blk.dt_tensor(), op=dist.ReduceOp.MIN, group=group)
+
+
+class DeviceRankBlock:
+    """This rank's block, resident on its GPU (libppmlr_b200)."""
+
+    def __init__(self, specs, partition, options, rank, ic, device):
+        import torch
+        from . import _native as N
+        from .api import _BOUNDARY, _PRECISION, check, host_block_state, layout
+        self.N = N
+        self.check_rc = check
+        blocks, _ = layout(specs, partition)
+        self.info = blocks[rank]
+        st = host_block_state(specs, partition, options, rank, ic)
+        d = N.BlockDesc()
+        g = options.ghost
+        self._geom = [np.ascontiguousarray(x) for x in st["centers"] + st["spacings"]]
+        for a in range(3):
+            d.n[a] = self.info.n[a]
+            d.lo[a] = self.info.lo[a]
+            d.centers[a] = self._geom[a].ctypes.data_as(C.POINTER(C.c_double))
+            d.spacings[a] = self._geom[3 + a].ctypes.data_as(C.POINTER(C.c_double))
+            d.physical[a][0] = int(self.info.neighbor[2 * a] < 0)
+            d.physical[a][1] = int(self.info.neighbor[2 * a + 1] < 0)
+        d.ghost = g
+        d.gamma, d.mu0, d.pressure_floor = options.gamma, options.mu0, options.pressure_floor
+        d.boundary = _BOUNDARY[options.boundary]
+        d.wind_rho, d.wind_p = options.wind.rho_sw, options.wind.p_sw
+        d.wind_v[:] = options.wind.v_sw
+        d.wind_imf[:] = options.wind.imf
+        d.with_dipole = int(options.with_dipole)
+        d.precision = _PRECISION[options.precision]
+        d.device = device
+        h = C.c_void_p()
+        check(N.lib.ppmlr_gpu_block_create(C.byref(d), C.byref(h)))
+        self.h = h
+        self.device = device
+        check(N.lib.ppmlr_gpu_block_set_stream(h, C.c_void_p(
+            torch.cuda.current_stream(device).cuda_stream)))
+        fi = st["frozen_idx"]
+        check(N.lib.ppmlr_gpu_block_upload(
+            h, st["fields"].ctypes.data_as(C.POINTER(C.c_double)),
+            None if st["bd"] is None else st["bd"].ctypes.data_as(C.POINTER(C.c_double)),
+            fi.ctypes.data_as(C.POINTER(C.c_int64)) if len(fi) else None,
+            st["frozen_states"].ctypes.data_as(C.POINTER(C.c_double)) if len(fi) else None,
+            len(fi)))
+        self._dt = torch.as_tensor(_CudaPtr(N.lib.ppmlr_gpu_block_dt_slot(h), 1),
+                                   device=f"cuda:{device}")
+        self.n = self.info.n
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.N.lib.ppmlr_gpu_block_destroy(self.h)
+            self.h = None
+
+    def dt_tensor(self):
+        return self._dt
+
+    def begin(self, cfl, first_step):
+        self.check_rc(self.N.lib.ppmlr_gpu_block_begin(self.h, cfl, first_step))
+
+    def pack_face(self, face, layers, buf):
+        self.check_rc(self.N.lib.ppmlr_gpu_block_pack_face(self.h, face, layers,
+                                                           C.c_void_p(buf.data_ptr())))
+
+    def unpack_face(self, face, layers, buf):
+        self.check_rc(self.N.lib.ppmlr_gpu_block_unpack_face(self.h, face, layers,
+                                                             C.c_void_p(buf.data_ptr())))
+
+    def fill_boundaries(self, mask, layers):
+        self.check_rc(self.N.lib.ppmlr_gpu_block_fill_boundaries(self.h, mask, layers))
+
+    def sweep_async(self, axis, s):
+        self.check_rc(self.N.lib.ppmlr_gpu_block_sweep_async(self.h, axis, s))
+
+    def end_step(self, cfl, with_sources):
+        self.check_rc(self.N.lib.ppmlr_gpu_block_end_step(self.h, cfl, int(with_sources)))
+
+    def check(self):
+        self.check_rc(self.N.lib.ppmlr_gpu_block_check(self.h))
+
+    def timing(self, enable):
+        sw, k, n = C.c_double(), C.c_double(), C.c_long()
+        self.check_rc(self.N.lib.ppmlr_gpu_block_timing(self.h, int(enable), C.byref(sw),
+                                                        C.byref(k), C.byref(n)))
+        return sw.value, k.value, n.value
+
+    def interior(self):
+        nx, ny, nz = self.n
+        out = np.zeros((nz, ny, nx, 8))
+        self.check_rc(self.N.lib.ppmlr_gpu_block_download_interior(
+            self.h, out.ctypes.data_as(C.POINTER(C.c_double))))
+        return out
+
+
+def run_rank(blk, ex, steps, first_step, cfl, with_sources, group=None, dt_ready=False):
+    if not dt_ready:
+        begin(blk, cfl, first_step, group)
+    for s in range(steps):
+        advance(blk, ex, first_step + s, cfl, with_sources, group)
+
+
+def bench_distributed(args, METRIC, UNIT, ALG, make_config, ClockSampler, fp64_peak_tflops,
+                      measured_peaks, cpu_baseline):
+    """bench.py's N-GPU arm: weak scaling, one 512^3 x-slab per rank."""
+    import torch
+    import torch.distributed as dist
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg, kind = make_config(args.config, world)
+    cfg.options.precision = args.precision
+    cfg.options.device = local
+    alg = ALG[kind]
+    blk = DeviceRankBlock(cfg.specs, cfg.partition, cfg.options, rank, cfg.ic, local)
+    ex = Exchanger(blk.info, blk.n, lambda n: torch.empty(n, dtype=torch.float64,
+                                                          device=f"cuda:{local}"))
+    cells_rank = blk.n[0] * blk.n[1] * blk.n[2]
+    cfl, srcs = cfg.options.cfl, cfg.options.with_sources
+    run_rank(blk, ex, args.warmup, 0, cfl, srcs)
+    torch.cuda.synchronize()
+    blk.timing(True)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        e0.record()
+        run_rank(blk, ex, args.steps, args.warmup, cfl, srcs, dt_ready=True)
+        e1.record()
+        e1.synchronize()
+    torch.cuda.synchronize()
+    dist.barrier()
+    blk.check()
+    ms = torch.tensor([e0.elapsed_time(e1)], device=f"cuda:{local}", dtype=torch.float64)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms = float(ms.item())
+    sweep_ms, kernels, launches = blk.timing(False)
+    value = cells_rank * world * args.steps / (ms * 1e-3)
+    if rank == 0:
+        peak = fp64_peak_tflops(local)
+        hbm, hbm_src = measured_peaks()
+        avg = sweep_ms * 1e-3 / max(launches, 1)
+        fb = cells_rank * alg["B_sweep"] / avg / (hbm * 1e9)
+        ff = cells_rank * alg["F_sweep"] / avg / (peak * 1e12)
+        bound = "fp64" if ff >= fb else "hbm"
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "precision": args.precision, "data": "synthetic (deterministic IC, no RNG)",
+            "config": {"workload": cfg.name, "grid": [int(s.cells) for s in cfg.specs],
+                       "cells_per_gpu": cells_rank, "partition": f"x-slab ({world},1,1)",
+                       "l2": "state >> L2"},
+            "clocks": clk.summary(), "gpu_launches": int(kernels),
+            "halo": {"messages": ex.messages, "bytes": ex.bytes_moved},
+            "roofline": {"bound": bound,
+                         "achieved": (cells_rank * alg["F_sweep"] / avg / 1e12) if bound == "fp64"
+                         else cells_rank * alg["B_sweep"] / avg / 1e9,
+                         "peak": peak if bound == "fp64" else hbm,
+                         "unit": "TFLOP/s" if bound == "fp64" else "GB/s",
+                         "frac": ff if bound == "fp64" else fb, "traffic": None,
+                         "frac_hbm": fb, "frac_fp64": ff, "peak_hbm_source": hbm_src},
+            "e2e": None,
+        }
+        print(json.dumps(line), flush=True)
+    blk.close()
+    dist.destroy_process_group()

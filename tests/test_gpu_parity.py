@@ -33,8 +33,8 @@ def _random_batch(rng, ns, n, bd_on, quiet=False):
     st = np.zeros((ns, nn, 8))
     st[..., 0] = rng.uniform(0.3, 2.5, (ns, nn))
     st[..., 7] = rng.uniform(0.1, 2.5, (ns, nn))
-    st[..., 1:4] = rng.uniform(-1, 1, (ns, nn, 3))
-    st[..., 4:7] = rng.uniform(-1.5, 1.5, (ns, nn, 3))
+    st[..., 1:4] = rng.uniform(-0.6, 0.6, (ns, nn, 3))
+    st[..., 4:7] = rng.uniform(-1.2, 1.2, (ns, nn, 3))
     if quiet:
         st[:, : nn // 2, 1:4] = 0.0
         st[:, : nn // 2, 4:] = st[:, :1, 4:]
@@ -54,12 +54,23 @@ def test_sweep_strips_bitwise_vs_oracle(gpu, oracle, direction, bd_on, n):
     c = oracle.consts()
     dt = min(oracle.orc_strip_max_dt(st[s], None if bd is None else bd[s], dx, n, 4, direction, c)
              for s in range(ns)) * 0.45
-    got = gpu.sweep_strips(st.copy(), bd, dx, n, 4, dt, direction)
+    wants, first_err = [], None
     for s in range(ns):
         want = st[s].copy()
-        oracle.orc_sweep_1d(want, None if bd is None else bd[s].copy(), dx, n, 4, dt, direction,
-                            c)
-        assert bits_equal(got[s], want), (s, np.abs(got[s] - want).max())
+        try:
+            oracle.orc_sweep_1d(want, None if bd is None else bd[s].copy(), dx, n, 4, dt,
+                                direction, c)
+        except oracle.OracleError as e:
+            first_err = first_err or e.msg
+        wants.append(want)
+    if first_err is not None:  # the GPU must fail the same way (first strip in order)
+        with pytest.raises(gpu.Error) as ex:
+            gpu.sweep_strips(st.copy(), bd, dx, n, 4, dt, direction)
+        assert str(ex.value) == first_err
+        return
+    got = gpu.sweep_strips(st.copy(), bd, dx, n, 4, dt, direction)
+    for s in range(ns):
+        assert bits_equal(got[s], wants[s]), (s, np.abs(got[s] - wants[s]).max())
 
 
 def test_sweep_strips_errors_match_reference(gpu, golden_strips):
