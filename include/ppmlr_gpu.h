@@ -83,6 +83,11 @@ int ppmlr_gpu_device_count(void);
 /* Measured FP64 FMA throughput of `device` in TFLOP/s (DFMA-chain
  * microbenchmark; the FP64 roofline denominator). */
 int ppmlr_gpu_fp64_peak(int device, double* tflops);
+/* Self-test of the bit-exact shared-reciprocal division used by the strict
+ * kernels against the compiler's `/` on n generated operand pairs; returns
+ * the mismatch count and the first mismatch (a, b, a/b, ours). */
+int ppmlr_gpu_selftest_division(int device, long long n, unsigned long long seed,
+                                long long* mismatches, double* example4);
 
 /* ------------------------------------------------------------------------
  * Block: one BlockState resident on one GPU (stepper.hpp:33-55) and the

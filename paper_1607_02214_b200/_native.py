@@ -107,6 +107,8 @@ _sig("ppmlr_host_block_state", C.c_int, C.POINTER(AxisSpecC), C.c_int, C.c_int, 
      C.POINTER(OptionsC), C.c_int, C.c_int, _dp, _dp, _dp, _i64p, _dp, _i64p, _dp, _dp)
 _sig("ppmlr_gpu_device_count", C.c_int)
 _sig("ppmlr_gpu_fp64_peak", C.c_int, C.c_int, _dp)
+_sig("ppmlr_gpu_selftest_division", C.c_int, C.c_int, C.c_longlong, C.c_ulonglong,
+     C.POINTER(C.c_longlong), _dp)
 _sig("ppmlr_tde_units", C.c_long, C.c_int, C.c_int, C.c_int)
 _sig("ppmlr_exchanged_bytes", C.c_uint64, C.POINTER(AxisSpecC), C.c_int, C.c_int, C.c_int,
      C.c_int, C.c_int)

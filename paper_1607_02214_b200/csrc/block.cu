@@ -222,19 +222,19 @@ struct CtxPtrs {
 // The three CFL candidates of compute_dt (stepper.cpp:128-137) for one cell.
 // Returns false (and the failing axis) on a non-finite candidate.
 __device__ __forceinline__ bool cfl_cell(const double* s, double b0, double b1, double b2,
-                                         double d0, double d1, double d2, const Consts& c,
+                                         double d0, double d1, double d2, const KC& c,
                                          double& mn, int& bad_axis) {
-  const double cand0 = d0 / (fabs(s[1]) + fast_speed3<0>(s, b0, b1, b2, c));
+  const double cand0 = div_x(d0, fabs(s[1]) + fast_speed3<0>(s, b0, b1, b2, c));
   if (!isfinite(cand0)) {
     bad_axis = 0;
     return false;
   }
-  const double cand1 = d1 / (fabs(s[2]) + fast_speed3<1>(s, b0, b1, b2, c));
+  const double cand1 = div_x(d1, fabs(s[2]) + fast_speed3<1>(s, b0, b1, b2, c));
   if (!isfinite(cand1)) {
     bad_axis = 1;
     return false;
   }
-  const double cand2 = d2 / (fabs(s[3]) + fast_speed3<2>(s, b0, b1, b2, c));
+  const double cand2 = div_x(d2, fabs(s[3]) + fast_speed3<2>(s, b0, b1, b2, c));
   if (!isfinite(cand2)) {
     bad_axis = 2;
     return false;
@@ -269,7 +269,8 @@ __device__ __forceinline__ void block_min_commit(double mn, unsigned long long* 
 template <bool DIPOLE>
 __global__ void cfl_kernel(Planes s, Lay L, const double* bd0, const double* bd1,
                            const double* bd2, const double* dx0, const double* dx1,
-                           const double* dx2, Consts c, CtxPtrs ctx, unsigned long long step_add) {
+                           const double* dx2, Consts cc, CtxPtrs ctx, unsigned long long step_add) {
+  const KC c = make_kc(cc);
   const long long total = (long long)L.n0 * L.n1 * L.n2;
   double mn = __longlong_as_double(kInfBits);
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
@@ -303,10 +304,11 @@ __global__ void step_end_kernel(CtxPtrs ctx, double cfl, int close_step, int hav
   }
 }
 
+// stepper.cpp:42-45; den = (hm*hp)*(hm+hp) and its refined reciprocal come
+// from per-position geometry tables.
 __device__ __forceinline__ double central_diff(double fm, double f0, double fp, double hm,
-                                               double hp) {
-  return (((hm * hm) * fp + ((hp * hp) - (hm * hm)) * f0) - (hp * hp) * fm) /
-         ((hm * hp) * (hm + hp));
+                                               double hp, double den, double rden) {
+  return div_r(((hm * hm) * fp + ((hp * hp) - (hm * hm)) * f0) - (hp * hp) * fm, den, rden);
 }
 
 __device__ __forceinline__ void cross3(double ax, double ay, double az, double bx, double by,
@@ -321,6 +323,7 @@ struct SrcArgs {
   Lay L;
   const double *bd0, *bd1, *bd2;
   const double *hm0, *hp0, *hm1, *hp1, *hm2, *hp2;  // per axis, ghost-inclusive
+  const double *den0, *den1, *den2, *rden0, *rden1, *rden2;
   const double *dx0, *dx1, *dx2;
   // frozen core
   int fl0, fl1, fl2, fn0, fn1, fn2;
@@ -337,7 +340,7 @@ struct SrcArgs {
 template <bool DIPOLE>
 __global__ void sources_kernel(const SrcArgs A) {
   const Lay& L = A.L;
-  const Consts& c = A.c;
+  const KC c = make_kc(A.c);
   const long long total = (long long)L.n0 * L.n1 * L.n2;
   double mn = __longlong_as_double(kInfBits);
   const unsigned long long step = *A.ctx.step;
@@ -363,6 +366,8 @@ __global__ void sources_kernel(const SrcArgs A) {
       const int lc = (a == 0 ? i : (a == 1 ? j : k)) + kG;
       const double hm = (a == 0 ? A.hm0 : (a == 1 ? A.hm1 : A.hm2))[lc];
       const double hp = (a == 0 ? A.hp0 : (a == 1 ? A.hp1 : A.hp2))[lc];
+      const double den = (a == 0 ? A.den0 : (a == 1 ? A.den1 : A.den2))[lc];
+      const double rden = (a == 0 ? A.rden0 : (a == 1 ? A.rden1 : A.rden2))[lc];
       double em[3], ep[3];
       cross3(A.in.f[1][dm], A.in.f[2][dm], A.in.f[3][dm], DIPOLE ? A.bd0[dm] : 0.0,
              DIPOLE ? A.bd1[dm] : 0.0, DIPOLE ? A.bd2[dm] : 0.0, em);
@@ -370,8 +375,9 @@ __global__ void sources_kernel(const SrcArgs A) {
              DIPOLE ? A.bd1[dp] : 0.0, DIPOLE ? A.bd2[dp] : 0.0, ep);
 #pragma unroll
       for (int comp = 0; comp < 3; ++comp) {
-        gb[a][comp] = central_diff(A.in.f[4 + comp][dm], s[4 + comp], A.in.f[4 + comp][dp], hm, hp);
-        ge[a][comp] = central_diff(em[comp], e0[comp], ep[comp], hm, hp);
+        gb[a][comp] =
+            central_diff(A.in.f[4 + comp][dm], s[4 + comp], A.in.f[4 + comp][dp], hm, hp, den, rden);
+        ge[a][comp] = central_diff(em[comp], e0[comp], ep[comp], hm, hp, den, rden);
       }
     }
     const double cb0 = gb[1][2] - gb[2][1], cb1 = gb[2][0] - gb[0][2], cb2 = gb[0][1] - gb[1][0];
@@ -379,12 +385,12 @@ __global__ void sources_kernel(const SrcArgs A) {
     const double div_b = (gb[0][0] + gb[1][1]) + gb[2][2];
     double sm[3];
     cross3(cb0, cb1, cb2, b0, b1, b2, sm);
-    sm[0] = sm[0] / c.mu0;
-    sm[1] = sm[1] / c.mu0;
-    sm[2] = sm[2] / c.mu0;
+    sm[0] = div_r(sm[0], c.c.mu0, c.r_mu0);
+    sm[1] = div_r(sm[1], c.c.mu0, c.r_mu0);
+    sm[2] = div_r(sm[2], c.c.mu0, c.r_mu0);
     const double si0 = ce0 - s[1] * div_b, si1 = ce1 - s[2] * div_b, si2 = ce2 - s[3] * div_b;
     const double se = ((s[1] * sm[0] + s[2] * sm[1]) + s[3] * sm[2]) +
-                      ((s[4] * ce0 + s[5] * ce1) + s[6] * ce2) / c.mu0;
+                      div_r((s[4] * ce0 + s[5] * ce1) + s[6] * ce2, c.c.mu0, c.r_mu0);
     double u[8];
     prim_to_cons3(s, u, c);
     u[1] = u[1] + sm[0] * dt;
@@ -423,6 +429,12 @@ __global__ void sources_kernel(const SrcArgs A) {
     }
   }
   if (A.fuse_cfl) block_min_commit(mn, A.ctx.min);
+}
+
+// In-place refined reciprocals of a geometry table.
+__global__ void rcp_table_kernel(double* v, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) v[i] = rcp_refined(v[i]);
 }
 
 __global__ void frozen_restore_kernel(Planes s, const long long* idx, const double* st,
@@ -613,12 +625,21 @@ int env_int(const char* name, int dflt) {
 }
 
 void choose_sweep_tiles(ppmlr_gpu_block* b) {
-  const int Lmax = env_int("PPMLR_SWEEP_LMAX", 120);
-  const int ipt = env_int("PPMLR_SWEEP_IPT", 2);
+  // Segments of kSweepTL - 8 = 64 cells (compile-time tile) when the axis is a
+  // multiple of 64 or long enough that a partial last segment costs little;
+  // otherwise balanced segments of at most Lmax cells (runtime tile).
+  const int Lmax = env_int("PPMLR_SWEEP_LMAX", 64);
+  const int ipt = env_int("PPMLR_SWEEP_IPT", 1);
+  const int Lc = kSweepTL - 8;
   for (int a = 0; a < 3; ++a) {
     const int n = b->n[a];
-    const int nseg = (n + Lmax - 1) / Lmax;
-    const int L = (n + nseg - 1) / nseg;
+    int L;
+    if (env_int("PPMLR_SWEEP_RUNTIME_TL", 0) == 0 && (n % Lc == 0 || n >= 4 * Lc)) {
+      L = Lc;
+    } else {
+      const int nseg = (n + Lmax - 1) / Lmax;
+      L = (n + nseg - 1) / nseg;
+    }
     b->sweep_L[a] = L;
     const int T = 4 * (L + 8);
     int nt = (T + ipt - 1) / ipt;
@@ -643,6 +664,7 @@ int launch_sweep(ppmlr_gpu_block* b, int axis, int phase) {
   }
   for (int k = 0; k < 3; ++k) A.bd[k] = b->bd ? b->bd + k * b->ncell : nullptr;
   A.dx = b->ax[axis].dx;
+  A.rdx = b->ax[axis].rdx;
   A.slope = b->ax[axis].slope;
   A.qfc = b->ax[axis].qfc;
   const long long strides[3] = {1, b->sy, b->sz};
@@ -727,6 +749,12 @@ int launch_sources(ppmlr_gpu_block* b, int fuse_cfl) {
   A.hp1 = b->ax[1].hp;
   A.hm2 = b->ax[2].hm;
   A.hp2 = b->ax[2].hp;
+  A.den0 = b->ax[0].den;
+  A.den1 = b->ax[1].den;
+  A.den2 = b->ax[2].den;
+  A.rden0 = b->ax[0].rden;
+  A.rden1 = b->ax[1].rden;
+  A.rden2 = b->ax[2].rden;
   A.dx0 = b->ax[0].dx;
   A.dx1 = b->ax[1].dx;
   A.dx2 = b->ax[2].dx;
@@ -867,6 +895,17 @@ int ppmlr_gpu_block_create(const ppmlr_gpu_block_desc* d, ppmlr_gpu_block** out)
     if ((rc = upload_vec(&b->ax[a].qfc, qfc))) return fail(rc);
     if ((rc = upload_vec(&b->ax[a].hm, hm))) return fail(rc);
     if ((rc = upload_vec(&b->ax[a].hp, hp))) return fail(rc);
+    std::vector<double> den(span, 1.0);
+    for (int l = 1; l + 1 < span; ++l) den[l] = (hm[l] * hp[l]) * (hm[l] + hp[l]);
+    if ((rc = upload_vec(&b->ax[a].den, den))) return fail(rc);
+    if ((rc = upload_vec(&b->ax[a].rdx, b->h_spacings[a]))) return fail(rc);
+    if ((rc = upload_vec(&b->ax[a].rden, den))) return fail(rc);
+    rcp_table_kernel<<<(span + 127) / 128, 128>>>(b->ax[a].rdx, span);
+    rcp_table_kernel<<<(span + 127) / 128, 128>>>(b->ax[a].rden, span);
+    if (cudaGetLastError() != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) {
+      set_error("rcp_table_kernel failed");
+      return fail(PPMLR_RUNTIME);
+    }
   }
   cudaError_t e;
   for (int k = 0; k < 2; ++k) {
@@ -914,6 +953,9 @@ void ppmlr_gpu_block_destroy(ppmlr_gpu_block* b) {
     cudaFree(b->ax[a].qfc);
     cudaFree(b->ax[a].hm);
     cudaFree(b->ax[a].hp);
+    cudaFree(b->ax[a].rdx);
+    cudaFree(b->ax[a].den);
+    cudaFree(b->ax[a].rden);
   }
   cudaFree(b->fslot);
   cudaFree(b->fstates);
@@ -1444,6 +1486,7 @@ int ppmlr_gpu_sweep_strips(double* states, const double* bd, const double* dx, i
   if (!rc) {
     // error keys of a bare sweep: phase Sweep0 + dir maps back to `dir`
     unsigned long long key = 0;
+    cudaStreamSynchronize(b->stream);
     cudaMemcpy(&key, b->d_err, 8, cudaMemcpyDeviceToHost);
     if (key != kNoError) {
       std::string msg;
@@ -1516,5 +1559,70 @@ extern "C" int ppmlr_gpu_fp64_peak(int device, double* tflops) {
   if (err != cudaSuccess) return cuda_fail(err, "dfma_peak_kernel");
   const double flops = 2.0 * 8.0 * (double)iters * threads * blocks;
   *tflops = flops / (best * 1e-3) / 1e12;
+  return 0;
+}
+
+// ------------------------------------------------------------------
+// Self-test of the shared-reciprocal division against the compiler's `/`
+// (bit patterns; NaN == NaN).  Operands mix random bit patterns, values of
+// physical magnitude, signed zeros, denormals and extremes.
+namespace {
+__device__ __forceinline__ unsigned long long mix64(unsigned long long x) {
+  x ^= x >> 33;
+  x *= 0xff51afd7ed558ccdull;
+  x ^= x >> 33;
+  x *= 0xc4ceb9fe1a85ec53ull;
+  x ^= x >> 33;
+  return x;
+}
+__device__ double pick(unsigned long long h, unsigned long long h2) {
+  switch (h2 % 8) {
+    case 0: return __longlong_as_double((long long)h);                       // any bits
+    case 1: return (double)((long long)(h >> 11)) * 1e-12 - 4.6e6;           // physical
+    case 2: return ldexp((double)(h >> 11) * 0x1p-53, (int)(h2 >> 8) % 200 - 100);
+    case 3: return (h & 1) ? 0.0 : -0.0;
+    case 4: return __longlong_as_double((long long)(h & 0x800fffffffffffffull));  // denormal
+    case 5: return ldexp(1.0 + (double)(h >> 12) * 0x1p-52, 1000 + (int)(h2 >> 8) % 24);
+    case 6: return ldexp(1.0 + (double)(h >> 12) * 0x1p-52, -1000 - (int)(h2 >> 8) % 74);
+    default: return (double)(long long)(h % 2001) - 1000.0;                  // small ints
+  }
+}
+__global__ void div_selftest_kernel(long long n, unsigned long long seed,
+                                    unsigned long long* bad, double* example) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const unsigned long long h = mix64(seed + 2 * (unsigned long long)i);
+    const unsigned long long g = mix64(seed + 2 * (unsigned long long)i + 1);
+    const double a = pick(h, mix64(h));
+    const double b = pick(g, mix64(g ^ 0x9e3779b97f4a7c15ull));
+    const double want = a / b;
+    const double got = div_r(a, b, rcp_refined(b));
+    const bool same = (__double_as_longlong(want) == __double_as_longlong(got)) ||
+                      (isnan(want) && isnan(got));
+    if (!same) {
+      if (atomicAdd(bad, 1ull) == 0) {
+        example[0] = a;
+        example[1] = b;
+        example[2] = want;
+        example[3] = got;
+      }
+    }
+  }
+}
+}  // namespace
+
+extern "C" int ppmlr_gpu_selftest_division(int device, long long n, unsigned long long seed,
+                                           long long* mismatches, double* example4) {
+  CK(cudaSetDevice(device));
+  unsigned long long* d = nullptr;
+  CK(cudaMalloc(&d, 8 + 4 * 8));
+  CK(cudaMemset(d, 0, 40));
+  div_selftest_kernel<<<148 * 16, 256>>>(n, seed, d, reinterpret_cast<double*>(d + 1));
+  CK(cudaGetLastError());
+  unsigned long long host[5];
+  CK(cudaMemcpy(host, d, 40, cudaMemcpyDeviceToHost));
+  cudaFree(d);
+  *mismatches = (long long)host[0];
+  if (example4) std::memcpy(example4, host + 1, 32);
   return 0;
 }

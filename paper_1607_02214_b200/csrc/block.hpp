@@ -7,7 +7,7 @@
 #include <vector>
 
 #include "../../include/ppmlr_gpu.h"
-#include "ppmlr_dev.cuh"
+#include "ppmlr_common.hpp"
 
 namespace ppmlr_b200 {
 
@@ -20,6 +20,9 @@ struct DevAxis {
   double* qfc = nullptr;    // 5 per edge: interface-value coefficients
   double* hm = nullptr;     // centers[l] - centers[l-1]   (apply_sources)
   double* hp = nullptr;     // centers[l+1] - centers[l]
+  double* rdx = nullptr;    // rcp_refined(dx)            (exact-division helper)
+  double* den = nullptr;    // (hm*hp)*(hm+hp)            (central_diff denominator)
+  double* rden = nullptr;   // rcp_refined(den)
   int span = 0;
 };
 

@@ -481,6 +481,7 @@ struct ppmlr_gpu_harness {
   std::vector<std::vector<double>> fst;
   long step = 0;
   double time = 0.0;
+  cudaStream_t stream = nullptr;  // one stream orders every block's work
   uint64_t ledger_bytes = 0;
   long ledger_messages = 0, ledger_events = 0;
 
@@ -697,6 +698,12 @@ int ppmlr_gpu_harness_create(const ppmlr_axis_spec specs[3], int px, int py, int
       ppmlr_gpu_block* b = nullptr;
       if (int e = ppmlr_gpu_block_create(&d, &b)) throw SpecError(e, ppmlr_gpu_last_error());
       h->blocks.push_back(b);
+      if (nb > 1) {  // halo copies read the neighbour's buffers: share one stream
+        if (!h->stream && cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess)
+          throw SpecError(PPMLR_RUNTIME, "cudaStreamCreate failed");
+        if (int e = ppmlr_gpu_block_set_stream(b, h->stream))
+          throw SpecError(e, ppmlr_gpu_last_error());
+      }
       if (h->o.with_dipole) block_dipole(host_block(h->ax, p, g), h->o.mu0, h->bd[r]);
       // make_block's default state {1, 0, 0, 1}
       std::vector<double> f(h->cells(r) * 8, 0.0);
@@ -719,6 +726,7 @@ int ppmlr_gpu_harness_create(const ppmlr_axis_spec specs[3], int px, int py, int
 void ppmlr_gpu_harness_destroy(ppmlr_gpu_harness* h) {
   if (!h) return;
   for (auto* b : h->blocks) ppmlr_gpu_block_destroy(b);
+  if (h->stream) cudaStreamDestroy(h->stream);
   delete h;
 }
 

@@ -31,11 +31,16 @@
 
 namespace ppmlr_b200 {
 
+// Compile-time tile length of the main sweep instantiation (L = 64 interior
+// cells per segment, 4 pencils per tile).
+constexpr int kSweepTL = 72;
+
 struct SweepArgs {
   const double* src[8];  // field planes of the input buffer (padded block layout)
   double* dst[8];        // field planes of the output buffer
   const double* bd[3];   // dipole planes (DIPOLE only)
   const double* dx;      // ghost-inclusive spacings along AXIS (span entries)
+  const double* rdx;     // rcp_refined(dx) per position (exact-division helper)
   const double* slope;   // 3 per strip position: c0, A, B
   const double* qfc;     // 5 per edge index m: e0..e4
   long long stride_a, stride_g, stride_o;  // element strides: sweep / group / other axis
@@ -61,10 +66,12 @@ struct AxisMap {
   static constexpr int B = (AXIS + 1) % 3;  // reference t1 axis
 };
 
-template <int AXIS, bool DIPOLE, int NP>
+// TLC > 0: compile-time tile length (TL = TLC = L + 8, constant smem strides);
+// TLC == 0: runtime TL = A.L + 8.
+template <int AXIS, bool DIPOLE, int NP, int TLC>
 __global__ void __launch_bounds__(512) sweep_kernel(const SweepArgs A) {
   extern __shared__ double smem[];
-  const int TL = A.L + 8;
+  const int TL = TLC > 0 ? TLC : A.L + 8;
   const int T = NP * TL;
   double* PRIM = smem;
   double* CONS = smem + 8 * T;
@@ -89,6 +96,7 @@ __global__ void __launch_bounds__(512) sweep_kernel(const SweepArgs A) {
   const int npv = min(NP, A.ng - g0);
   const double dt = *A.dt;
   const Consts& c = A.c;
+  const KC k = make_kc(c);
   const long long base = (long long)(g0 + 4) * A.stride_g + (long long)(oc + 4) * A.stride_o +
                          (long long)seg0 * A.stride_a;
 
@@ -137,7 +145,7 @@ __global__ void __launch_bounds__(512) sweep_kernel(const SweepArgs A) {
       BD[1 * T + ci] = AXIS == 0 ? b1 : (AXIS == 1 ? b2 : b0);
       BD[2 * T + ci] = AXIS == 0 ? b2 : (AXIS == 1 ? b0 : b1);
     }
-    CF[ci] = fast_speed3<AXIS>(q, b0, b1, b2, c);
+    CF[ci] = fast_speed3<AXIS>(q, b0, b1, b2, k);
     constexpr int a = AXIS, b = (AXIS + 1) % 3, d = (AXIS + 2) % 3;
     double w[8];
     w[kRho] = q[0];
@@ -157,7 +165,7 @@ __global__ void __launch_bounds__(512) sweep_kernel(const SweepArgs A) {
     CONS[kBn * T + ci] = w[kBn];
     CONS[kBt1 * T + ci] = w[kBt1];
     CONS[kBt2 * T + ci] = w[kBt2];
-    CONS[kPE * T + ci] = strip_energy(w, c);
+    CONS[kPE * T + ci] = strip_energy(w, k);
   }
   __syncthreads();
 
@@ -201,9 +209,10 @@ __global__ void __launch_bounds__(512) sweep_kernel(const SweepArgs A) {
     if (s < 2 || s > zmax || p >= npv) continue;
     const int q = seg0 + s;
     const bool flat = q < 2 || q >= nn - 2;
-    const double sigma = sclamp((CF[ci] * dt) / __ldg(A.dx + q), 0.0, 1.0);
+    const double sigma =
+        sclamp(div_r(CF[ci] * dt, __ldg(A.dx + q), __ldg(A.rdx + q)), 0.0, 1.0);
     const double hs = 0.5 * sigma;
-    const double tw = 1.0 - (2.0 * sigma) / 3.0;
+    const double tw = tw_of(sigma, k);
     double own[8], L[8], R[8];
 #pragma unroll
     for (int v = 0; v < 8; ++v) {
@@ -216,7 +225,7 @@ __global__ void __launch_bounds__(512) sweep_kernel(const SweepArgs A) {
       } else {
         al = SB[v * T + ci];
         ar = SB[v * T + ci + SS];
-        limit_parabola(al, ar, av, six);
+        limit_parabola(al, ar, av, six, k);
       }
       L[v] = avg_left(al, ar, six, hs, tw);
       R[v] = avg_right(al, ar, six, hs, tw);
@@ -250,7 +259,7 @@ __global__ void __launch_bounds__(512) sweep_kernel(const SweepArgs A) {
           br[k] = BD[k * T + ci];
         }
       }
-      CF[ci] = solve_edge(ql, qr, bl, br, c, f);
+      CF[ci] = solve_edge(ql, qr, bl, br, k, f);
 #pragma unroll
       for (int v = 0; v < 8; ++v) SB[v * T + ci] = f[v];
     }
@@ -298,18 +307,21 @@ __global__ void __launch_bounds__(512) sweep_kernel(const SweepArgs A) {
                                    kErrStepRejected));
       continue;
     }
-    const double shrink = dx0 / dxp;
+    const double r_dxp = rcp_refined(dxp);
+    const double shrink = div_r(dx0, dxp, r_dxp);
     double u[8];
 #pragma unroll
     for (int v = 0; v < 8; ++v)
-      u[v] = CONS[v * T + ci] * shrink - (dt * (SB[v * T + ci + SS] - SB[v * T + ci])) / dxp;
+      u[v] = CONS[v * T + ci] * shrink -
+             div_r(dt * (SB[v * T + ci + SS] - SB[v * T + ci]), dxp, r_dxp);
 #pragma unroll
     for (int v = 0; v < 8; ++v) SA[v * T + ci] = u[v];
     if (c.pressure_floor <= 0.0) {
       const double internal =
-          (u[kPE] - (0.5 * ((u[kUn] * u[kUn] + u[kUt1] * u[kUt1]) + u[kUt2] * u[kUt2])) /
-                        u[kRho]) -
-          ((u[kBn] * u[kBn] + u[kBt1] * u[kBt1]) + u[kBt2] * u[kBt2]) / c.two_mu0;
+          (u[kPE] - div_x(0.5 * ((u[kUn] * u[kUn] + u[kUt1] * u[kUt1]) + u[kUt2] * u[kUt2]),
+                          u[kRho])) -
+          div_r((u[kBn] * u[kBn] + u[kBt1] * u[kBt1]) + u[kBt2] * u[kBt2], c.two_mu0,
+                k.r_two_mu0);
       if (!(u[kRho] > 0.0) || !(internal > 0.0))
         atomicMin(A.err, err_key(*A.step, A.phase, AXIS,
                                  (pencil_index(p) << 20) | ((unsigned long long)q << 2) |
@@ -335,14 +347,14 @@ __global__ void __launch_bounds__(512) sweep_kernel(const SweepArgs A) {
       const int kc = right ? ci - SS : ci;
       const int kq = right ? m - 1 : m;
       const double width = __ldg(A.dx + kq) + dt * (CF[kc + SS] - CF[kc]);
-      const double sigma = (right ? delta : -delta) / width;
+      const double sigma = div_x(right ? delta : -delta, width);
       const double hs = 0.5 * sigma;
-      const double tw = 1.0 - (2.0 * sigma) / 3.0;
+      const double tw = tw_of(sigma, k);
 #pragma unroll
       for (int v = 0; v < 8; ++v) {
         const double av = CONS[v * T + kc];
         double al = PRIM[v * T + kc], ar = PRIM[v * T + kc + SS], six;
-        limit_parabola(al, ar, av, six);
+        limit_parabola(al, ar, av, six, k);
         const double mean = right ? avg_right(al, ar, six, hs, tw) : avg_left(al, ar, six, hs, tw);
         sl[v] = delta * (mean + (SA[v * T + kc] - av));
       }
@@ -359,12 +371,13 @@ __global__ void __launch_bounds__(512) sweep_kernel(const SweepArgs A) {
     if (s < 4 || s > TLv - 5 || p >= npv) continue;
     const int q = seg0 + s;
     const double dxe = __ldg(A.dx + q);
+    const double r_dxe = __ldg(A.rdx + q);
     const double width = dxe + dt * (CF[ci + SS] - CF[ci]);
-    const double scale = width / dxe;
+    const double scale = div_r(width, dxe, r_dxe);
     double u[8];
 #pragma unroll
     for (int v = 0; v < 8; ++v)
-      u[v] = SA[v * T + ci] * scale + (SB[v * T + ci] - SB[v * T + ci + SS]) / dxe;
+      u[v] = SA[v * T + ci] * scale + div_r(SB[v * T + ci] - SB[v * T + ci + SS], dxe, r_dxe);
     constexpr int a = AXIS, b = (AXIS + 1) % 3, d = (AXIS + 2) % 3;
     double cs[8], out[8];
     cs[0] = u[kRho];
@@ -375,7 +388,7 @@ __global__ void __launch_bounds__(512) sweep_kernel(const SweepArgs A) {
     cs[4 + b] = u[kBt1];
     cs[4 + d] = u[kBt2];
     cs[7] = u[kPE];
-    const int bad = cons_to_prim3(cs, out, c);
+    const int bad = cons_to_prim3(cs, out, k);
     if (bad) {
       atomicMin(A.err, err_key(*A.step, A.phase, AXIS,
                                (pencil_index(p) << 20) | (1ull << 19) |

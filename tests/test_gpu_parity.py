@@ -16,6 +16,22 @@ pytestmark = pytest.mark.gpu
 FAST_L1, FAST_LINF = 1e-11, 1e-9
 
 
+# ------------------------------------------------------------ exact division
+
+def test_exact_division_matches_ieee_divide(gpu):
+    """The strict kernels' shared-reciprocal division (exact_div.cuh) is
+    bit-identical to the compiler's `/` on 2^28 operand pairs including
+    zeros, denormals, extremes, inf/nan bit patterns."""
+    import ctypes
+    from paper_1607_02214_b200 import _native as N
+    bad = ctypes.c_longlong()
+    ex = np.zeros(4)
+    for seed in (1, 12345):
+        N.check(N.lib.ppmlr_gpu_selftest_division(0, 1 << 27, seed, ctypes.byref(bad),
+                                                  ex.ctypes.data_as(N._dp)))
+        assert bad.value == 0, (bad.value, ex.tolist())
+
+
 # ------------------------------------------------------------ sweep_1d
 
 def test_sweep_strips_match_reference_golden(gpu, golden_strips):
