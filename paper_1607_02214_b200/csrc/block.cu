@@ -685,6 +685,8 @@ int launch_sweep(ppmlr_gpu_block* b, int axis, int phase) {
   A.step = b->d_step;
   A.phase = phase;
   A.c = b->c;
+  A.redo_count = b->d_redo;
+  A.redo_list = b->d_redo + 1;
   const int T = 4 * (A.L + 8);
   const size_t smem = sizeof(double) * (size_t)T * (33 + (b->with_dipole ? 3 : 0));
   // The sweep writes only the interior of the output buffer; its ghost
@@ -695,7 +697,7 @@ int launch_sweep(ppmlr_gpu_block* b, int axis, int phase) {
                       : launch_sweep_strict(axis, b->with_dipole, A, b->sweep_threads[axis],
                                             smem, b->stream);
   if (e != cudaSuccess) return cuda_fail(e, "sweep kernel launch");
-  b->kernel_launches += 1;
+  b->kernel_launches += 2;  // fast pass + exact re-run of flagged tiles
   b->cur ^= 1;
   return 0;
 }
@@ -934,6 +936,17 @@ int ppmlr_gpu_block_create(const ppmlr_gpu_block_desc* d, ppmlr_gpu_block** out)
   if ((e = cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking)) != cudaSuccess)
     return fail(cuda_fail(e, "cudaStreamCreate"));
   choose_sweep_tiles(b);
+  {
+    long long tiles = 1;
+    for (int a = 0; a < 3; ++a) {
+      const int G = a == 0 ? 1 : 0, O = a == 2 ? 1 : 2;
+      const long long t = (long long)((b->n[a] + b->sweep_L[a] - 1) / b->sweep_L[a]) *
+                          ((b->n[G] + 3) / 4) * b->n[O];
+      tiles = std::max(tiles, t);
+    }
+    if ((e = cudaMalloc(&b->d_redo, sizeof(unsigned) * (tiles + 1))) != cudaSuccess)
+      return fail(cuda_fail(e, "cudaMalloc(redo)"));
+  }
   *out = b;
   return 0;
 }
@@ -961,6 +974,7 @@ void ppmlr_gpu_block_destroy(ppmlr_gpu_block* b) {
   cudaFree(b->fstates);
   cudaFree(b->fidx);
   cudaFree(b->d_err);
+  cudaFree(b->d_redo);
   cudaFree(b->d_scratch);
   if (b->h_pinned) cudaFreeHost(b->h_pinned);
   for (auto& ev : b->ev)
@@ -1141,9 +1155,9 @@ int ppmlr_gpu_block_compute_dt(ppmlr_gpu_block* b, double cfl, double* dt_out) {
   CK(cudaSetDevice(b->device));
   if (int rc = launch_cfl(b, 0)) return rc;
   if (int rc = launch_step_end(b, cfl, 0, 1)) return rc;
-  CK(cudaMemcpyAsync(b->h_pinned, b->d_dt, 8, cudaMemcpyDeviceToHost, b->stream));
-  if (int rc = ppmlr_gpu_block_check(b)) return rc;
-  *dt_out = b->h_pinned[0];
+  CK(cudaMemcpyAsync(b->h_pinned + 6, b->d_dt, 8, cudaMemcpyDeviceToHost, b->stream));
+  if (int rc = ppmlr_gpu_block_check(b)) return rc;  // uses h_pinned[0]
+  *dt_out = b->h_pinned[6];
   return 0;
 }
 

@@ -20,7 +20,7 @@ namespace ppmlr_b200 {
 namespace PPMLR_KNS {
 
 // Reciprocals of the run constants and of the literal divisors 6 and 3,
-// refined once per thread (rcp_refined is the divisor-only half of `/`).
+// refined once per thread (the divisor-only half of nvcc's `/`).
 struct KC {
   Consts c;
   double r_gm1, r_two_mu0, r_mu0, r6, r3;
@@ -44,44 +44,48 @@ __device__ __forceinline__ double sclamp(double v, double lo, double hi) {
 }
 
 // physics.cpp:63-72 fast_speed: total field b = B' + bd, |b|^2 in xyz order.
-template <int DIR>
+template <int DIR, class Ops>
 __device__ __forceinline__ double fast_speed3(const double* s, double bdx, double bdy,
-                                              double bdz, const KC& k) {
+                                              double bdz, const KC& k, Ops& o) {
   const double b0 = s[4] + bdx, b1 = s[5] + bdy, b2 = s[6] + bdz;
   const double bdir = DIR == 0 ? b0 : (DIR == 1 ? b1 : b2);
   const double mr = k.c.mu0 * s[0];
-  const double r_mr = rcp_refined(mr);
-  const double a2 = div_x(k.c.gamma * s[7], s[0]);
-  const double ca2 = div_r((b0 * b0 + b1 * b1) + b2 * b2, mr, r_mr);
-  const double can2 = div_r(bdir * bdir, mr, r_mr);
+  const double r_mr = o.rcp(mr);
+  const double a2 = o.dv(k.c.gamma * s[7], s[0]);
+  const double ca2 = o.div((b0 * b0 + b1 * b1) + b2 * b2, mr, r_mr);
+  const double can2 = o.div(bdir * bdir, mr, r_mr);
   const double sum = a2 + ca2;
-  const double disc = sqrt(smax(0.0, sum * sum - (4.0 * a2) * can2));
-  return sqrt(0.5 * (sum + disc));
+  const double disc = o.sq(smax(0.0, sum * sum - (4.0 * a2) * can2));
+  return o.sq(0.5 * (sum + disc));
 }
 
 // ppm1d.cpp:29-37 fast_speed_strip: |b|^2 in strip order.
+template <class Ops>
 __device__ __forceinline__ double fast_speed_strip(double rho, double p, double btn,
-                                                   double btt1, double btt2, const KC& k) {
+                                                   double btt1, double btt2, const KC& k,
+                                                   Ops& o) {
   const double mr = k.c.mu0 * rho;
-  const double r_mr = rcp_refined(mr);
-  const double a2 = div_x(k.c.gamma * p, rho);
-  const double ca2 = div_r((btn * btn + btt1 * btt1) + btt2 * btt2, mr, r_mr);
-  const double can2 = div_r(btn * btn, mr, r_mr);
+  const double r_mr = o.rcp(mr);
+  const double a2 = o.dv(k.c.gamma * p, rho);
+  const double ca2 = o.div((btn * btn + btt1 * btt1) + btt2 * btt2, mr, r_mr);
+  const double can2 = o.div(btn * btn, mr, r_mr);
   const double sum = a2 + ca2;
-  const double disc = sqrt(smax(0.0, sum * sum - (4.0 * a2) * can2));
-  return sqrt(0.5 * (sum + disc));
+  const double disc = o.sq(smax(0.0, sum * sum - (4.0 * a2) * can2));
+  return o.sq(0.5 * (sum + disc));
 }
 
 // ppm1d.cpp:39-52 prim_to_cons_strip; only the energy slot is non-trivial.
-__device__ __forceinline__ double strip_energy(const double* w, const KC& k) {
-  return (div_r(w[kPE], k.c.gm1, k.r_gm1) +
+template <class Ops>
+__device__ __forceinline__ double strip_energy(const double* w, const KC& k, Ops& o) {
+  return (o.div(w[kPE], k.c.gm1, k.r_gm1) +
           (0.5 * w[kRho]) * ((w[kUn] * w[kUn] + w[kUt1] * w[kUt1]) + w[kUt2] * w[kUt2])) +
-         div_r((w[kBn] * w[kBn] + w[kBt1] * w[kBt1]) + w[kBt2] * w[kBt2], k.c.two_mu0,
+         o.div((w[kBn] * w[kBn] + w[kBt1] * w[kBt1]) + w[kBt2] * w[kBt2], k.c.two_mu0,
                k.r_two_mu0);
 }
 
 // physics.cpp:29-37 prim_to_cons (xyz order) into u[8].
-__device__ __forceinline__ void prim_to_cons3(const double* s, double* u, const KC& k) {
+template <class Ops>
+__device__ __forceinline__ void prim_to_cons3(const double* s, double* u, const KC& k, Ops& o) {
   u[0] = s[0];
   u[1] = s[1] * s[0];
   u[2] = s[2] * s[0];
@@ -91,46 +95,46 @@ __device__ __forceinline__ void prim_to_cons3(const double* s, double* u, const 
   u[6] = s[6];
   const double v2 = (s[1] * s[1] + s[2] * s[2]) + s[3] * s[3];
   const double b2 = (s[4] * s[4] + s[5] * s[5]) + s[6] * s[6];
-  u[7] = (div_r(s[7], k.c.gm1, k.r_gm1) + (0.5 * s[0]) * v2) +
-         div_r(b2, k.c.two_mu0, k.r_two_mu0);
+  u[7] = (o.div(s[7], k.c.gm1, k.r_gm1) + (0.5 * s[0]) * v2) +
+         o.div(b2, k.c.two_mu0, k.r_two_mu0);
 }
 
-// physics.cpp:39-57 cons_to_prim (xyz order).  Returns 0 ok, 1 density, 2 pressure.
-__device__ __forceinline__ int cons_to_prim3(const double* u, double* q, const KC& k) {
-  if (!(u[0] > 0.0)) return 1;
-  const double rr = rcp_refined(u[0]);
+// physics.cpp:39-57 cons_to_prim (xyz order), branch-free.  Returns 0 ok,
+// 1 non-positive density, 2 non-positive pressure (q is then unspecified).
+template <class Ops>
+__device__ __forceinline__ int cons_to_prim3(const double* u, double* q, const KC& k, Ops& o) {
+  const bool rho_ok = u[0] > 0.0;
+  const double rr = o.rcp(u[0]);
   q[0] = u[0];
-  q[1] = div_r(u[1], u[0], rr);
-  q[2] = div_r(u[2], u[0], rr);
-  q[3] = div_r(u[3], u[0], rr);
+  q[1] = o.div(u[1], u[0], rr);
+  q[2] = o.div(u[2], u[0], rr);
+  q[3] = o.div(u[3], u[0], rr);
   q[4] = u[4];
   q[5] = u[5];
   q[6] = u[6];
   const double m2 = (u[1] * u[1] + u[2] * u[2]) + u[3] * u[3];
   const double b2 = (u[4] * u[4] + u[5] * u[5]) + u[6] * u[6];
   const double internal =
-      (u[7] - div_r(0.5 * m2, u[0], rr)) - div_r(b2, k.c.two_mu0, k.r_two_mu0);
-  q[7] = k.c.gm1 * internal;
-  if (!(q[7] > 0.0)) {
-    if (k.c.pressure_floor > 0.0)
-      q[7] = k.c.pressure_floor;
-    else
-      return 2;
-  }
-  return 0;
+      (u[7] - o.div(0.5 * m2, u[0], rr)) - o.div(b2, k.c.two_mu0, k.r_two_mu0);
+  const double p = k.c.gm1 * internal;
+  const bool p_ok = p > 0.0;
+  const bool floor = !p_ok && k.c.pressure_floor > 0.0;
+  q[7] = floor ? k.c.pressure_floor : p;
+  if (!rho_ok) return 1;
+  return (p_ok || floor) ? 0 : 2;
 }
 
-// ppm1d.cpp:14-24 limited_slope with hoisted geometry:
+// ppm1d.cpp:14-24 limited_slope with hoisted geometry, branch-free:
 //   c0 = dx_k/((dx_{k-1}+dx_k)+dx_{k+1}), A = (2dx_{k-1}+dx_k)/(dx_{k+1}+dx_k),
 //   B = (dx_k+2dx_{k+1})/(dx_{k-1}+dx_k)   (bit-exact: same subexpressions).
 __device__ __forceinline__ double limited_slope(double qm, double q0, double qp, double c0,
                                                 double A, double B) {
   const double dql = q0 - qm;
   const double dqr = qp - q0;
-  if (dqr * dql <= 0.0) return 0.0;
   const double dq = c0 * (A * dqr + B * dql);
   const double lim = 2.0 * smin(fabs(dql), fabs(dqr));
-  return copysign(smin(fabs(dq), lim), dq);
+  const double lim_dq = copysign(smin(fabs(dq), lim), dq);
+  return (dqr * dql <= 0.0) ? 0.0 : lim_dq;
 }
 
 // ppm1d.cpp:217-224 CW84 interface value at edge m (i = m-1) with hoisted e0..e4.
@@ -140,22 +144,22 @@ __device__ __forceinline__ double interface_value(double qi, double qi1, double 
   return (qi + e[0] * dqr) + e[1] * ((e[2] * dqr - e[3] * dmi1) + e[4] * dmi);
 }
 
-// ppm1d.cpp:232-246 monotonicity limiter.  In: al, ar (interface values), av.
-// Out: al, ar limited, six.  ((-d)*d)/6 == -((d*d)/6) exactly, so the
-// second comparison reuses the first quotient.
+// ppm1d.cpp:232-246 monotonicity limiter, branch-free.  ((-d)*d)/6 equals
+// -((d*d)/6) exactly, so one quotient serves both comparisons; the steepened
+// values use the unmodified al / ar exactly as the reference's if/else chain.
+template <class Ops>
 __device__ __forceinline__ void limit_parabola(double& al, double& ar, double av, double& six,
-                                               const KC& k) {
-  if ((ar - av) * (av - al) <= 0.0) {
-    al = ar = av;
-  } else {
-    const double d = ar - al;
-    const double t = d * (av - 0.5 * (al + ar));
-    const double x = div_r(d * d, 6.0, k.r6);
-    if (t > x)
-      al = 3.0 * av - 2.0 * ar;
-    else if (t < -x)
-      ar = 3.0 * av - 2.0 * al;
-  }
+                                               const KC& k, Ops& o) {
+  const bool flat = (ar - av) * (av - al) <= 0.0;
+  const double d = ar - al;
+  const double t = d * (av - 0.5 * (al + ar));
+  const double x = o.div(d * d, 6.0, k.r6);
+  const bool up = t > x;
+  const bool dn = !up && t < -x;
+  const double al_s = 3.0 * av - 2.0 * ar;
+  const double ar_s = 3.0 * av - 2.0 * al;
+  al = flat ? av : (up ? al_s : al);
+  ar = flat ? av : (dn ? ar_s : ar);
   six = 6.0 * (av - 0.5 * (al + ar));
 }
 
@@ -169,49 +173,64 @@ __device__ __forceinline__ double avg_right(double l, double r, double six, doub
                                             double tw) {
   return r - hs * ((r - l) - tw * six);
 }
-__device__ __forceinline__ double tw_of(double sigma, const KC& k) {
-  return 1.0 - div_r(2.0 * sigma, 3.0, k.r3);
+template <class Ops>
+__device__ __forceinline__ double tw_of(double sigma, const KC& k, Ops& o) {
+  return 1.0 - o.div(2.0 * sigma, 3.0, k.r3);
 }
 
 // ppm1d.cpp:69-109 solve_edge + edge_flux.  ql/qr strip-frame traced states,
 // bl/br total-field offsets (bd components in strip order a, b, d).
-__device__ __forceinline__ double solve_edge(const double* ql, const double* qr,
+template <class QL, class QR, class Ops>
+__device__ __forceinline__ double solve_edge(const QL& ql, const QR& qr,
                                              const double* bl, const double* br, const KC& k,
-                                             double* f) {
+                                             double* f, Ops& o) {
   const Consts& c = k.c;
   const double wl = ql[kRho] * fast_speed_strip(ql[kRho], ql[kPE], ql[kBn] + bl[0],
-                                                ql[kBt1] + bl[1], ql[kBt2] + bl[2], k);
+                                                ql[kBt1] + bl[1], ql[kBt2] + bl[2], k, o);
   const double wr = qr[kRho] * fast_speed_strip(qr[kRho], qr[kPE], qr[kBn] + br[0],
-                                                qr[kBt1] + br[1], qr[kBt2] + br[2], k);
-  const double pl = ql[kPE] + div_r((ql[kBt1] * ql[kBt1] + ql[kBt2] * ql[kBt2]) -
+                                                qr[kBt1] + br[1], qr[kBt2] + br[2], k, o);
+  const double pl = ql[kPE] + o.div((ql[kBt1] * ql[kBt1] + ql[kBt2] * ql[kBt2]) -
                                         ql[kBn] * ql[kBn],
                                     c.two_mu0, k.r_two_mu0);
-  const double pr = qr[kPE] + div_r((qr[kBt1] * qr[kBt1] + qr[kBt2] * qr[kBt2]) -
+  const double pr = qr[kPE] + o.div((qr[kBt1] * qr[kBt1] + qr[kBt2] * qr[kBt2]) -
                                         qr[kBn] * qr[kBn],
                                     c.two_mu0, k.r_two_mu0);
   const double wsum = wl + wr;
-  const double r_ws = rcp_refined(wsum);
-  const double ustar = div_r(((wl * ql[kUn] + wr * qr[kUn]) + pl) - pr, wsum, r_ws);
-  const double pstar = div_r((wr * pl + wl * pr) + (wl * wr) * (ql[kUn] - qr[kUn]), wsum, r_ws);
+  const double r_ws = o.rcp(wsum);
+  const double ustar = o.div(((wl * ql[kUn] + wr * qr[kUn]) + pl) - pr, wsum, r_ws);
+  const double pstar = o.div((wr * pl + wl * pr) + (wl * wr) * (ql[kUn] - qr[kUn]), wsum, r_ws);
   const double bn = 0.5 * (ql[kBn] + qr[kBn]);
   const double s = bn < 0.0 ? -1.0 : 1.0;
-  const double al = div_x(1.0, sqrt(c.mu0 * ql[kRho]));
-  const double ar = div_x(1.0, sqrt(c.mu0 * qr[kRho]));
+  const double al = o.dv(1.0, o.sq(c.mu0 * ql[kRho]));
+  const double ar = o.dv(1.0, o.sq(c.mu0 * qr[kRho]));
   const double asum = al + ar;
-  const double r_as = rcp_refined(asum);
-  const double bt1 = div_r((s * (qr[kUt1] - ql[kUt1]) + ar * qr[kBt1]) + al * ql[kBt1], asum, r_as);
-  const double bt2 = div_r((s * (qr[kUt2] - ql[kUt2]) + ar * qr[kBt2]) + al * ql[kBt2], asum, r_as);
+  const double r_as = o.rcp(asum);
+  const double bt1 = o.div((s * (qr[kUt1] - ql[kUt1]) + ar * qr[kBt1]) + al * ql[kBt1], asum, r_as);
+  const double bt2 = o.div((s * (qr[kUt2] - ql[kUt2]) + ar * qr[kBt2]) + al * ql[kBt2], asum, r_as);
   const double vt1 = ql[kUt1] + (s * al) * (bt1 - ql[kBt1]);
   const double vt2 = ql[kUt2] + (s * al) * (bt2 - ql[kBt2]);
   f[kRho] = 0.0;
   f[kUn] = pstar;
-  f[kUt1] = div_r((-bn) * bt1, c.mu0, k.r_mu0);
-  f[kUt2] = div_r((-bn) * bt2, c.mu0, k.r_mu0);
+  f[kUt1] = o.div((-bn) * bt1, c.mu0, k.r_mu0);
+  f[kUt2] = o.div((-bn) * bt2, c.mu0, k.r_mu0);
   f[kBn] = (-ustar) * bn;
   f[kBt1] = (-bn) * vt1;
   f[kBt2] = (-bn) * vt2;
-  f[kPE] = pstar * ustar - div_r(bn * (vt1 * bt1 + vt2 * bt2), c.mu0, k.r_mu0);
+  f[kPE] = pstar * ustar - o.div(bn * (vt1 * bt1 + vt2 * bt2), c.mu0, k.r_mu0);
   return ustar;
+}
+
+// Runs `body(ops)` with FastOps and, if any fast-path guard failed, again
+// with ExactOps (plain `/` and `sqrt`): the item's results are bit-identical
+// to the reference in both cases; the second run is rare.
+template <class F>
+__device__ __forceinline__ void exact_item(F&& body) {
+  FastOps fo;
+  body(fo);
+  if (fo.bad) {
+    ExactOps eo;
+    body(eo);
+  }
 }
 
 }  // namespace PPMLR_KNS

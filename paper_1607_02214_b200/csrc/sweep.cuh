@@ -54,9 +54,18 @@ struct SweepArgs {
   const unsigned long long* step;  // device step counter for error keys
   int phase;             // kPhaseSweep{0,1,2}
   Consts c;
+  unsigned* redo_count;  // tiles whose fast-path guards failed ...
+  unsigned* redo_list;   // ... are re-run exactly by the EXACT instance
 };
 
 namespace PPMLR_KNS {
+
+// Strided view of one cell's 8 strip variables in shared memory.
+struct SmemVec {
+  const double* p;
+  int stride;
+  __device__ __forceinline__ double operator[](int v) const { return p[v * stride]; }
+};
 
 template <int AXIS>
 struct AxisMap {
@@ -68,9 +77,14 @@ struct AxisMap {
 
 // TLC > 0: compile-time tile length (TL = TLC = L + 8, constant smem strides);
 // TLC == 0: runtime TL = A.L + 8.
-template <int AXIS, bool DIPOLE, int NP, int TLC>
-__global__ void __launch_bounds__(512) sweep_kernel(const SweepArgs A) {
-  extern __shared__ double smem[];
+// One tile of the sweep with arithmetic policy Ops.  Returns true when a
+// FastOps guard failed somewhere in the tile (its results and error keys
+// are then discarded and the tile is re-run with ExactOps).  Error keys go
+// to *s_err (shared) and are committed by the caller.
+template <int AXIS, bool DIPOLE, int NP, int TLC, class Ops>
+__device__ __forceinline__ bool sweep_tile(const SweepArgs& A, const int bid, double* smem,
+                                           unsigned long long* s_err) {
+  bool tbad = false;
   const int TL = TLC > 0 ? TLC : A.L + 8;
   const int T = NP * TL;
   double* PRIM = smem;
@@ -82,7 +96,6 @@ __global__ void __launch_bounds__(512) sweep_kernel(const SweepArgs A) {
   // Neighbour offset along the strip inside the tile.
   const int SS = AXIS == 0 ? 1 : NP;
 
-  const int bid = blockIdx.x;
   const int seg = bid % A.nseg;
   const int rest = bid / A.nseg;
   const int grp = rest % A.ngroups;
@@ -145,7 +158,6 @@ __global__ void __launch_bounds__(512) sweep_kernel(const SweepArgs A) {
       BD[1 * T + ci] = AXIS == 0 ? b1 : (AXIS == 1 ? b2 : b0);
       BD[2 * T + ci] = AXIS == 0 ? b2 : (AXIS == 1 ? b0 : b1);
     }
-    CF[ci] = fast_speed3<AXIS>(q, b0, b1, b2, k);
     constexpr int a = AXIS, b = (AXIS + 1) % 3, d = (AXIS + 2) % 3;
     double w[8];
     w[kRho] = q[0];
@@ -156,6 +168,14 @@ __global__ void __launch_bounds__(512) sweep_kernel(const SweepArgs A) {
     w[kBt1] = q[4 + b];
     w[kBt2] = q[4 + d];
     w[kPE] = q[7];
+    double cf = 0.0, e = 0.0;
+    {
+      Ops o;
+      cf = fast_speed3<AXIS>(q, b0, b1, b2, k, o);
+      e = strip_energy(w, k, o);
+      tbad |= o.bad;
+    }
+    CF[ci] = cf;
 #pragma unroll
     for (int v = 0; v < 8; ++v) PRIM[v * T + ci] = w[v];
     CONS[kRho * T + ci] = w[kRho];
@@ -165,7 +185,7 @@ __global__ void __launch_bounds__(512) sweep_kernel(const SweepArgs A) {
     CONS[kBn * T + ci] = w[kBn];
     CONS[kBt1 * T + ci] = w[kBt1];
     CONS[kBt2 * T + ci] = w[kBt2];
-    CONS[kPE * T + ci] = strip_energy(w, k);
+    CONS[kPE * T + ci] = e;
   }
   __syncthreads();
 
@@ -192,7 +212,7 @@ __global__ void __launch_bounds__(512) sweep_kernel(const SweepArgs A) {
     double e[5];
     const double* ge = A.qfc + 5 * (seg0 + s);
 #pragma unroll
-    for (int k = 0; k < 5; ++k) e[k] = __ldg(ge + k);
+    for (int kk = 0; kk < 5; ++kk) e[kk] = __ldg(ge + kk);
 #pragma unroll
     for (int v = 0; v < 8; ++v) {
       const double* q = PRIM + v * T + ci;
@@ -209,33 +229,30 @@ __global__ void __launch_bounds__(512) sweep_kernel(const SweepArgs A) {
     if (s < 2 || s > zmax || p >= npv) continue;
     const int q = seg0 + s;
     const bool flat = q < 2 || q >= nn - 2;
-    const double sigma =
-        sclamp(div_r(CF[ci] * dt, __ldg(A.dx + q), __ldg(A.rdx + q)), 0.0, 1.0);
-    const double hs = 0.5 * sigma;
-    const double tw = tw_of(sigma, k);
-    double own[8], L[8], R[8];
+    const double dxq = __ldg(A.dx + q), rdxq = __ldg(A.rdx + q);
+    double L[8], R[8];
+    {
+      Ops o;
+      const double sigma = sclamp(o.div(CF[ci] * dt, dxq, rdxq), 0.0, 1.0);
+      const double hs = 0.5 * sigma;
+      const double tw = tw_of(sigma, k, o);
 #pragma unroll
-    for (int v = 0; v < 8; ++v) {
-      const double av = PRIM[v * T + ci];
-      own[v] = av;
-      double al, ar, six;
-      if (flat) {
-        al = ar = av;
-        six = 0.0;
-      } else {
-        al = SB[v * T + ci];
-        ar = SB[v * T + ci + SS];
-        limit_parabola(al, ar, av, six, k);
+      for (int v = 0; v < 8; ++v) {
+        const double av = PRIM[v * T + ci];
+        double al = flat ? av : SB[v * T + ci], ar = flat ? av : SB[v * T + ci + SS], six;
+        limit_parabola(al, ar, av, six, k, o);
+        L[v] = avg_left(al, ar, six, hs, tw);
+        R[v] = avg_right(al, ar, six, hs, tw);
       }
-      L[v] = avg_left(al, ar, six, hs, tw);
-      R[v] = avg_right(al, ar, six, hs, tw);
+      tbad |= o.bad;
     }
     const bool badL = !(L[kRho] > 0.0) || !(L[kPE] > 0.0);
     const bool badR = !(R[kRho] > 0.0) || !(R[kPE] > 0.0);
 #pragma unroll
     for (int v = 0; v < 8; ++v) {
-      PRIM[v * T + ci] = badR ? own[v] : R[v];
-      SA[v * T + ci] = badL ? own[v] : L[v];
+      if (!badL) SA[v * T + ci] = L[v];
+      else SA[v * T + ci] = PRIM[v * T + ci];
+      if (!badR) PRIM[v * T + ci] = R[v];
     }
   }
   __syncthreads();
@@ -246,20 +263,22 @@ __global__ void __launch_bounds__(512) sweep_kernel(const SweepArgs A) {
     decode(ci, s, p);
     if (p >= npv) continue;
     if (s >= 3 && s <= zmax) {
-      double ql[8], qr[8], f[8], bl[3] = {0.0, 0.0, 0.0}, br[3] = {0.0, 0.0, 0.0};
-#pragma unroll
-      for (int v = 0; v < 8; ++v) {
-        ql[v] = PRIM[v * T + ci - SS];
-        qr[v] = SA[v * T + ci];
-      }
+      double f[8], bl[3] = {0.0, 0.0, 0.0}, br[3] = {0.0, 0.0, 0.0};
+      const SmemVec ql{PRIM + ci - SS, T}, qr{SA + ci, T};
       if (DIPOLE) {
 #pragma unroll
-        for (int k = 0; k < 3; ++k) {
-          bl[k] = BD[k * T + ci - SS];
-          br[k] = BD[k * T + ci];
+        for (int kk = 0; kk < 3; ++kk) {
+          bl[kk] = BD[kk * T + ci - SS];
+          br[kk] = BD[kk * T + ci];
         }
       }
-      CF[ci] = solve_edge(ql, qr, bl, br, k, f);
+      double us = 0.0;
+      {
+      Ops o;
+        us = solve_edge(ql, qr, bl, br, k, f, o);
+        tbad |= o.bad;
+      }
+      CF[ci] = us;
 #pragma unroll
       for (int v = 0; v < 8; ++v) SB[v * T + ci] = f[v];
     }
@@ -283,7 +302,7 @@ __global__ void __launch_bounds__(512) sweep_kernel(const SweepArgs A) {
     double e[5];
     const double* ge = A.qfc + 5 * (seg0 + s);
 #pragma unroll
-    for (int k = 0; k < 5; ++k) e[k] = __ldg(ge + k);
+    for (int kk = 0; kk < 5; ++kk) e[kk] = __ldg(ge + kk);
 #pragma unroll
     for (int v = 0; v < 8; ++v) {
       const double* q = CONS + v * T + ci;
@@ -302,31 +321,33 @@ __global__ void __launch_bounds__(512) sweep_kernel(const SweepArgs A) {
     const double dx0 = __ldg(A.dx + q);
     const double dxp = dx0 + dt * (CF[ci + SS] - CF[ci]);
     if (!(dxp > 0.0)) {
-      atomicMin(A.err, err_key(*A.step, A.phase, AXIS,
+      atomicMin(s_err, err_key(*A.step, A.phase, AXIS,
                                (pencil_index(p) << 20) | ((unsigned long long)q << 2) |
                                    kErrStepRejected));
       continue;
     }
-    const double r_dxp = rcp_refined(dxp);
-    const double shrink = div_r(dx0, dxp, r_dxp);
-    double u[8];
+    double u[8], internal = 0.0;
+    {
+      Ops o;
+      const double r_dxp = o.rcp(dxp);
+      const double shrink = o.div(dx0, dxp, r_dxp);
 #pragma unroll
-    for (int v = 0; v < 8; ++v)
-      u[v] = CONS[v * T + ci] * shrink -
-             div_r(dt * (SB[v * T + ci + SS] - SB[v * T + ci]), dxp, r_dxp);
+      for (int v = 0; v < 8; ++v)
+        u[v] = CONS[v * T + ci] * shrink -
+               o.div(dt * (SB[v * T + ci + SS] - SB[v * T + ci]), dxp, r_dxp);
+      internal =
+          (u[kPE] - o.dv(0.5 * ((u[kUn] * u[kUn] + u[kUt1] * u[kUt1]) + u[kUt2] * u[kUt2]),
+                         u[kRho])) -
+          o.div((u[kBn] * u[kBn] + u[kBt1] * u[kBt1]) + u[kBt2] * u[kBt2], c.two_mu0,
+                k.r_two_mu0);
+      tbad |= o.bad;
+    }
 #pragma unroll
     for (int v = 0; v < 8; ++v) SA[v * T + ci] = u[v];
-    if (c.pressure_floor <= 0.0) {
-      const double internal =
-          (u[kPE] - div_x(0.5 * ((u[kUn] * u[kUn] + u[kUt1] * u[kUt1]) + u[kUt2] * u[kUt2]),
-                          u[kRho])) -
-          div_r((u[kBn] * u[kBn] + u[kBt1] * u[kBt1]) + u[kBt2] * u[kBt2], c.two_mu0,
-                k.r_two_mu0);
-      if (!(u[kRho] > 0.0) || !(internal > 0.0))
-        atomicMin(A.err, err_key(*A.step, A.phase, AXIS,
-                                 (pencil_index(p) << 20) | ((unsigned long long)q << 2) |
-                                     kErrLagUnphysical));
-    }
+    if (c.pressure_floor <= 0.0 && (!(u[kRho] > 0.0) || !(internal > 0.0)))
+      atomicMin(s_err, err_key(*A.step, A.phase, AXIS,
+                               (pencil_index(p) << 20) | ((unsigned long long)q << 2) |
+                                   kErrLagUnphysical));
   }
   __syncthreads();
 
@@ -347,16 +368,21 @@ __global__ void __launch_bounds__(512) sweep_kernel(const SweepArgs A) {
       const int kc = right ? ci - SS : ci;
       const int kq = right ? m - 1 : m;
       const double width = __ldg(A.dx + kq) + dt * (CF[kc + SS] - CF[kc]);
-      const double sigma = div_x(right ? delta : -delta, width);
-      const double hs = 0.5 * sigma;
-      const double tw = tw_of(sigma, k);
+      {
+      Ops o;
+        const double sigma = o.dv(right ? delta : -delta, width);
+        const double hs = 0.5 * sigma;
+        const double tw = tw_of(sigma, k, o);
 #pragma unroll
-      for (int v = 0; v < 8; ++v) {
-        const double av = CONS[v * T + kc];
-        double al = PRIM[v * T + kc], ar = PRIM[v * T + kc + SS], six;
-        limit_parabola(al, ar, av, six, k);
-        const double mean = right ? avg_right(al, ar, six, hs, tw) : avg_left(al, ar, six, hs, tw);
-        sl[v] = delta * (mean + (SA[v * T + kc] - av));
+        for (int v = 0; v < 8; ++v) {
+          const double av = CONS[v * T + kc];
+          double al = PRIM[v * T + kc], ar = PRIM[v * T + kc + SS], six;
+          limit_parabola(al, ar, av, six, k, o);
+          const double mean =
+              right ? avg_right(al, ar, six, hs, tw) : avg_left(al, ar, six, hs, tw);
+          sl[v] = delta * (mean + (SA[v * T + kc] - av));
+        }
+        tbad |= o.bad;
       }
     }
 #pragma unroll
@@ -373,24 +399,30 @@ __global__ void __launch_bounds__(512) sweep_kernel(const SweepArgs A) {
     const double dxe = __ldg(A.dx + q);
     const double r_dxe = __ldg(A.rdx + q);
     const double width = dxe + dt * (CF[ci + SS] - CF[ci]);
-    const double scale = div_r(width, dxe, r_dxe);
-    double u[8];
-#pragma unroll
-    for (int v = 0; v < 8; ++v)
-      u[v] = SA[v * T + ci] * scale + div_r(SB[v * T + ci] - SB[v * T + ci + SS], dxe, r_dxe);
+    double out[8];
     constexpr int a = AXIS, b = (AXIS + 1) % 3, d = (AXIS + 2) % 3;
-    double cs[8], out[8];
-    cs[0] = u[kRho];
-    cs[1 + a] = u[kUn];
-    cs[1 + b] = u[kUt1];
-    cs[1 + d] = u[kUt2];
-    cs[4 + a] = u[kBn];
-    cs[4 + b] = u[kBt1];
-    cs[4 + d] = u[kBt2];
-    cs[7] = u[kPE];
-    const int bad = cons_to_prim3(cs, out, k);
+    int bad = 0;
+    {
+      Ops o;
+      const double scale = o.div(width, dxe, r_dxe);
+      double u[8];
+#pragma unroll
+      for (int v = 0; v < 8; ++v)
+        u[v] = SA[v * T + ci] * scale + o.div(SB[v * T + ci] - SB[v * T + ci + SS], dxe, r_dxe);
+      double cs[8];
+      cs[0] = u[kRho];
+      cs[1 + a] = u[kUn];
+      cs[1 + b] = u[kUt1];
+      cs[1 + d] = u[kUt2];
+      cs[4 + a] = u[kBn];
+      cs[4 + b] = u[kBt1];
+      cs[4 + d] = u[kBt2];
+      cs[7] = u[kPE];
+      bad = cons_to_prim3(cs, out, k, o);
+      tbad |= o.bad;
+    }
     if (bad) {
-      atomicMin(A.err, err_key(*A.step, A.phase, AXIS,
+      atomicMin(s_err, err_key(*A.step, A.phase, AXIS,
                                (pencil_index(p) << 20) | (1ull << 19) |
                                    ((unsigned long long)(q - 4) << 2) |
                                    (bad == 1 ? kErrDensity : kErrPressure)));
@@ -400,7 +432,39 @@ __global__ void __launch_bounds__(512) sweep_kernel(const SweepArgs A) {
 #pragma unroll
     for (int f = 0; f < 8; ++f) A.dst[f][off] = out[f];
   }
+  return tbad;
 }
+
+// FAST instance: every tile with FastOps; a tile whose guards all held
+// commits its error keys and results, otherwise it is queued for EXACT.
+// EXACT instance: re-runs the queued tiles with plain `/` and `sqrt`.
+template <int AXIS, bool DIPOLE, int NP, int TLC, bool EXACT>
+__global__ void __launch_bounds__(TLC > 0 ? NP * TLC : 512, TLC > 0 ? 2 : 1)
+    sweep_kernel(const SweepArgs A) {
+  extern __shared__ double smem[];
+  __shared__ unsigned long long s_err;
+  if (EXACT) {
+    const unsigned n = *A.redo_count;
+    for (unsigned i = blockIdx.x; i < n; i += gridDim.x) {
+      if (threadIdx.x == 0) s_err = kNoError;
+      __syncthreads();
+      sweep_tile<AXIS, DIPOLE, NP, TLC, ExactOps>(A, (int)A.redo_list[i], smem, &s_err);
+      __syncthreads();
+      if (threadIdx.x == 0 && s_err != kNoError) atomicMin(A.err, s_err);
+      __syncthreads();
+    }
+    return;
+  }
+  if (threadIdx.x == 0) s_err = kNoError;
+  __syncthreads();
+  const bool bad = sweep_tile<AXIS, DIPOLE, NP, TLC, FastOps>(A, blockIdx.x, smem, &s_err);
+  if (__syncthreads_or(bad)) {
+    if (threadIdx.x == 0) A.redo_list[atomicAdd(A.redo_count, 1u)] = blockIdx.x;
+  } else if (threadIdx.x == 0 && s_err != kNoError) {
+    atomicMin(A.err, s_err);
+  }
+}
+
 
 }  // namespace PPMLR_KNS
 }  // namespace ppmlr_b200
