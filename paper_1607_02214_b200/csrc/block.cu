@@ -221,25 +221,31 @@ struct CtxPtrs {
 
 // The three CFL candidates of compute_dt (stepper.cpp:128-137) for one cell.
 // Returns false (and the failing axis) on a non-finite candidate.
+template <class Ops>
+__device__ __forceinline__ void cfl_cands(const double* s, double b0, double b1, double b2,
+                                          double d0, double d1, double d2, const KC& c, Ops& o,
+                                          double* cand) {
+  cand[0] = o.dv(d0, fabs(s[1]) + fast_speed3<0>(s, b0, b1, b2, c, o));
+  cand[1] = o.dv(d1, fabs(s[2]) + fast_speed3<1>(s, b0, b1, b2, c, o));
+  cand[2] = o.dv(d2, fabs(s[3]) + fast_speed3<2>(s, b0, b1, b2, c, o));
+}
+
 __device__ __forceinline__ bool cfl_cell(const double* s, double b0, double b1, double b2,
                                          double d0, double d1, double d2, const KC& c,
                                          double& mn, int& bad_axis) {
-  const double cand0 = div_x(d0, fabs(s[1]) + fast_speed3<0>(s, b0, b1, b2, c));
-  if (!isfinite(cand0)) {
-    bad_axis = 0;
-    return false;
+  double cand[3];
+  FastOps fo;
+  cfl_cands(s, b0, b1, b2, d0, d1, d2, c, fo, cand);
+  if (fo.bad) {
+    ExactOps eo;
+    cfl_cands(s, b0, b1, b2, d0, d1, d2, c, eo, cand);
   }
-  const double cand1 = div_x(d1, fabs(s[2]) + fast_speed3<1>(s, b0, b1, b2, c));
-  if (!isfinite(cand1)) {
-    bad_axis = 1;
-    return false;
-  }
-  const double cand2 = div_x(d2, fabs(s[3]) + fast_speed3<2>(s, b0, b1, b2, c));
-  if (!isfinite(cand2)) {
-    bad_axis = 2;
-    return false;
-  }
-  mn = smin(smin(smin(mn, cand0), cand1), cand2);
+  for (int a = 0; a < 3; ++a)
+    if (!isfinite(cand[a])) {
+      bad_axis = a;
+      return false;
+    }
+  mn = smin(smin(smin(mn, cand[0]), cand[1]), cand[2]);
   return true;
 }
 
@@ -306,9 +312,10 @@ __global__ void step_end_kernel(CtxPtrs ctx, double cfl, int close_step, int hav
 
 // stepper.cpp:42-45; den = (hm*hp)*(hm+hp) and its refined reciprocal come
 // from per-position geometry tables.
+template <class Ops>
 __device__ __forceinline__ double central_diff(double fm, double f0, double fp, double hm,
-                                               double hp, double den, double rden) {
-  return div_r(((hm * hm) * fp + ((hp * hp) - (hm * hm)) * f0) - (hp * hp) * fm, den, rden);
+                                               double hp, double den, double rden, Ops& o) {
+  return o.div(((hm * hm) * fp + ((hp * hp) - (hm * hm)) * f0) - (hp * hp) * fm, den, rden);
 }
 
 __device__ __forceinline__ void cross3(double ax, double ay, double az, double bx, double by,
@@ -356,6 +363,9 @@ __global__ void sources_kernel(const SrcArgs A) {
     for (int f = 0; f < 8; ++f) s[f] = A.in.f[f][d];
     const double b0 = DIPOLE ? A.bd0[d] : 0.0, b1 = DIPOLE ? A.bd1[d] : 0.0,
                  b2 = DIPOLE ? A.bd2[d] : 0.0;
+    double q[8];
+    int bad = 0;
+    auto compute = [&](auto& o) {
     double gb[3][3], ge[3][3];
     double e0[3];
     cross3(s[1], s[2], s[3], b0, b1, b2, e0);
@@ -376,8 +386,8 @@ __global__ void sources_kernel(const SrcArgs A) {
 #pragma unroll
       for (int comp = 0; comp < 3; ++comp) {
         gb[a][comp] =
-            central_diff(A.in.f[4 + comp][dm], s[4 + comp], A.in.f[4 + comp][dp], hm, hp, den, rden);
-        ge[a][comp] = central_diff(em[comp], e0[comp], ep[comp], hm, hp, den, rden);
+            central_diff(A.in.f[4 + comp][dm], s[4 + comp], A.in.f[4 + comp][dp], hm, hp, den, rden, o);
+        ge[a][comp] = central_diff(em[comp], e0[comp], ep[comp], hm, hp, den, rden, o);
       }
     }
     const double cb0 = gb[1][2] - gb[2][1], cb1 = gb[2][0] - gb[0][2], cb2 = gb[0][1] - gb[1][0];
@@ -385,14 +395,14 @@ __global__ void sources_kernel(const SrcArgs A) {
     const double div_b = (gb[0][0] + gb[1][1]) + gb[2][2];
     double sm[3];
     cross3(cb0, cb1, cb2, b0, b1, b2, sm);
-    sm[0] = div_r(sm[0], c.c.mu0, c.r_mu0);
-    sm[1] = div_r(sm[1], c.c.mu0, c.r_mu0);
-    sm[2] = div_r(sm[2], c.c.mu0, c.r_mu0);
+    sm[0] = o.div(sm[0], c.c.mu0, c.r_mu0);
+    sm[1] = o.div(sm[1], c.c.mu0, c.r_mu0);
+    sm[2] = o.div(sm[2], c.c.mu0, c.r_mu0);
     const double si0 = ce0 - s[1] * div_b, si1 = ce1 - s[2] * div_b, si2 = ce2 - s[3] * div_b;
     const double se = ((s[1] * sm[0] + s[2] * sm[1]) + s[3] * sm[2]) +
-                      div_r((s[4] * ce0 + s[5] * ce1) + s[6] * ce2, c.c.mu0, c.r_mu0);
+                      o.div((s[4] * ce0 + s[5] * ce1) + s[6] * ce2, c.c.mu0, c.r_mu0);
     double u[8];
-    prim_to_cons3(s, u, c);
+    prim_to_cons3(s, u, c, o);
     u[1] = u[1] + sm[0] * dt;
     u[2] = u[2] + sm[1] * dt;
     u[3] = u[3] + sm[2] * dt;
@@ -400,8 +410,16 @@ __global__ void sources_kernel(const SrcArgs A) {
     u[5] = u[5] + si1 * dt;
     u[6] = u[6] + si2 * dt;
     u[7] = u[7] + dt * se;
-    double q[8];
-    const int bad = cons_to_prim3(u, q, c);
+    bad = cons_to_prim3(u, q, c, o);
+    };
+    {
+      FastOps fo;
+      compute(fo);
+      if (fo.bad) {
+        ExactOps eo;
+        compute(eo);
+      }
+    }
     if (bad) {
       atomicMin(A.ctx.err, err_key(step, kPhaseSources, 0,
                                    ((unsigned long long)t << 2) |
