@@ -340,20 +340,29 @@ struct SrcArgs {
   Consts c;
   CtxPtrs ctx;
   int fuse_cfl;
+  unsigned* redo_count;
+  unsigned* redo_list;
+  unsigned redo_cap;
 };
 
 // apply_sources (stepper.cpp:141-200) + restore_frozen_core (:284-286) +
 // the next step's compute_dt (:119-139), one thread per interior cell.
-template <bool DIPOLE>
-__global__ void sources_kernel(const SrcArgs A) {
+// FAST: every cell with FastOps; cells whose fast-path guards failed are
+// queued (redo list; on overflow the EXACT pass covers every cell) and left
+// to EXACT, which recomputes them with plain `/` and `sqrt`.
+template <bool DIPOLE, bool EXACT>
+__global__ void __launch_bounds__(256, 2) sources_kernel(const SrcArgs A) {
   const Lay& L = A.L;
   const KC c = make_kc(A.c);
   const long long total = (long long)L.n0 * L.n1 * L.n2;
   double mn = __longlong_as_double(kInfBits);
   const unsigned long long step = *A.ctx.step;
   const double dt = *A.ctx.dt;
-  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
-       t += (long long)gridDim.x * blockDim.x) {
+  const bool all = EXACT && *A.redo_count > A.redo_cap;
+  const long long n_items = EXACT ? (all ? total : (long long)*A.redo_count) : total;
+  for (long long it = blockIdx.x * (long long)blockDim.x + threadIdx.x; it < n_items;
+       it += (long long)gridDim.x * blockDim.x) {
+    const long long t = (EXACT && !all) ? (long long)A.redo_list[it] : it;
     const int i = (int)(t % L.n0);
     const int j = (int)((t / L.n0) % L.n1);
     const int k = (int)(t / ((long long)L.n0 * L.n1));
@@ -412,12 +421,16 @@ __global__ void sources_kernel(const SrcArgs A) {
     u[7] = u[7] + dt * se;
     bad = cons_to_prim3(u, q, c, o);
     };
-    {
+    if (EXACT) {
+      ExactOps eo;
+      compute(eo);
+    } else {
       FastOps fo;
       compute(fo);
       if (fo.bad) {
-        ExactOps eo;
-        compute(eo);
+        const unsigned slot = atomicAdd(A.redo_count, 1u);
+        if (slot < A.redo_cap) A.redo_list[slot] = (unsigned)t;
+        continue;
       }
     }
     if (bad) {
@@ -790,12 +803,20 @@ int launch_sources(ppmlr_gpu_block* b, int fuse_cfl) {
   A.c = b->c;
   A.ctx = ctx_of(b);
   A.fuse_cfl = fuse_cfl;
+  A.redo_count = b->d_redo;
+  A.redo_list = b->d_redo + 1;
+  A.redo_cap = b->redo_cap;
   const long long work = (long long)b->n[0] * b->n[1] * b->n[2];
-  if (b->with_dipole)
-    sources_kernel<true><<<grid_for(work), 256, 0, b->stream>>>(A);
-  else
-    sources_kernel<false><<<grid_for(work), 256, 0, b->stream>>>(A);
+  CK(cudaMemsetAsync(b->d_redo, 0, sizeof(unsigned), b->stream));
+  if (b->with_dipole) {
+    sources_kernel<true, false><<<grid_for(work), 256, 0, b->stream>>>(A);
+    sources_kernel<true, true><<<148, 256, 0, b->stream>>>(A);
+  } else {
+    sources_kernel<false, false><<<grid_for(work), 256, 0, b->stream>>>(A);
+    sources_kernel<false, true><<<148, 256, 0, b->stream>>>(A);
+  }
   CK(cudaGetLastError());
+  b->kernel_launches += 1;
   b->kernel_launches += 1;
   b->cur ^= 1;
   return 0;
@@ -962,7 +983,9 @@ int ppmlr_gpu_block_create(const ppmlr_gpu_block_desc* d, ppmlr_gpu_block** out)
                           ((b->n[G] + 3) / 4) * b->n[O];
       tiles = std::max(tiles, t);
     }
-    if ((e = cudaMalloc(&b->d_redo, sizeof(unsigned) * (tiles + 1))) != cudaSuccess)
+    const long long cells = (long long)b->n[0] * b->n[1] * b->n[2];
+    b->redo_cap = (unsigned)std::max<long long>(tiles, std::min<long long>(cells, 1 << 22));
+    if ((e = cudaMalloc(&b->d_redo, sizeof(unsigned) * ((size_t)b->redo_cap + 1))) != cudaSuccess)
       return fail(cuda_fail(e, "cudaMalloc(redo)"));
   }
   *out = b;

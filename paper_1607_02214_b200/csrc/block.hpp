@@ -76,7 +76,8 @@ struct ppmlr_gpu_block {
   long long* fidx = nullptr;   // device linear indices (for the standalone restore)
   // device scalars
   unsigned long long* d_err = nullptr;   // first-failure key
-  unsigned* d_redo = nullptr;            // [0] count, [1..] tiles re-run exactly
+  unsigned* d_redo = nullptr;            // [0] count, [1..] tiles/cells re-run exactly
+  unsigned redo_cap = 0;
   unsigned long long* d_step = nullptr;  // step counter for keys (relative)
   unsigned long long* d_min = nullptr;   // CFL min as ordered bits
   double* d_dt = nullptr;                // dt in use

@@ -435,7 +435,13 @@ __device__ __forceinline__ bool sweep_tile(const SweepArgs& A, const int bid, do
   return tbad;
 }
 
-// FAST instance: every tile with FastOps; a tile whose guards all held
+#ifdef PPMLR_FAST_MATH
+using MainOps = FastMathOps;  // tolerance-gated fast mode
+#else
+using MainOps = FastOps;      // bit-exact replay of nvcc's fast paths
+#endif
+
+// FAST instance: every tile with MainOps; a tile whose guards all held
 // commits its error keys and results, otherwise it is queued for EXACT.
 // EXACT instance: re-runs the queued tiles with plain `/` and `sqrt`.
 template <int AXIS, bool DIPOLE, int NP, int TLC, bool EXACT>
@@ -457,7 +463,7 @@ __global__ void __launch_bounds__(TLC > 0 ? NP * TLC : 512, TLC > 0 ? 2 : 1)
   }
   if (threadIdx.x == 0) s_err = kNoError;
   __syncthreads();
-  const bool bad = sweep_tile<AXIS, DIPOLE, NP, TLC, FastOps>(A, blockIdx.x, smem, &s_err);
+  const bool bad = sweep_tile<AXIS, DIPOLE, NP, TLC, MainOps>(A, blockIdx.x, smem, &s_err);
   if (__syncthreads_or(bad)) {
     if (threadIdx.x == 0) A.redo_list[atomicAdd(A.redo_count, 1u)] = blockIdx.x;
   } else if (threadIdx.x == 0 && s_err != kNoError) {

@@ -314,3 +314,30 @@ def test_conservation_periodic_at_scale(gpu):
     h.run(10)
     m1, e1 = totals()
     assert max(abs(m1 - m0) / m0, abs(e1 - e0) / e0) < 1e-11
+
+
+# ------------------------------------------------------------ fast mode
+
+@pytest.mark.parametrize("cfg,steps", [("blast", 12), ("orszag_tang", 12),
+                                       ("magnetosphere_small", 8), ("briowu", 40)])
+def test_fast_mode_within_tolerance_of_strict(gpu, cfg, steps):
+    """The tolerance gate of the fast build: after N
+    full steps, per-field relative L1 <= 1e-11 and Linf <= 1e-9 against the
+    bit-exact strict path (itself pinned to the reference)."""
+    from paper_1607_02214_b200 import configs
+    mk = {"briowu": lambda **kw: configs.brio_wu(nx=128, **kw),
+          "orszag_tang": lambda **kw: configs.orszag_tang(n=64, **kw),
+          "blast": lambda **kw: configs.blast(n=32, radius=0.2, **kw),
+          "magnetosphere_small": lambda **kw: configs.magnetosphere_small(**kw)}[cfg]
+    res = {}
+    for prec in ("strict", "fast"):
+        c = mk(precision=prec)
+        h = _harness(gpu, c.specs, c.options, c.ic)
+        h.run(steps)
+        res[prec] = h.gather_interior()
+    a, b = res["fast"].reshape(-1, 8), res["strict"].reshape(-1, 8)
+    n = a.shape[0]
+    d = np.abs(a - b)
+    l1 = d.sum(0) / np.maximum(np.abs(b).sum(0), n * 1e-12)
+    linf = d.max(0) / np.maximum(np.abs(b).max(0), 1e-12)
+    assert l1.max() <= FAST_L1 and linf.max() <= FAST_LINF, (l1.max(), linf.max())
