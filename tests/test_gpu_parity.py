@@ -341,3 +341,41 @@ def test_fast_mode_within_tolerance_of_strict(gpu, cfg, steps):
     l1 = d.sum(0) / np.maximum(np.abs(b).sum(0), n * 1e-12)
     linf = d.max(0) / np.maximum(np.abs(b).max(0), 1e-12)
     assert l1.max() <= FAST_L1 and linf.max() <= FAST_LINF, (l1.max(), linf.max())
+
+
+def test_pack_unpack_slabs_in_reference_order(gpu):
+    """Device halo slabs equal the reference HaloSlab payload order
+    (exchange.cpp:30-51: t2 -> t1 -> layer -> 8 scalars) and unpack lands
+    them in the receiver's opposite ghost shell (exchange.cpp:53-82)."""
+    import ctypes
+    import torch
+    from paper_1607_02214_b200 import _native as N
+    from paper_1607_02214_b200.api import AxisSpec, HarnessOptions
+    specs = [AxisSpec.uniform(-1, 1, 10), AxisSpec.uniform(-1, 1, 6), AxisSpec.uniform(-1, 1, 8)]
+    h = _harness(gpu, specs, HarnessOptions(), (gpu.IC_PARTITION, ()))
+    blk = h.block(0)
+    full = blk.download()  # (S2, S1, S0, 8), ghost 4
+    g, n = 4, (10, 6, 8)
+    for face in range(6):
+        a = face // 2
+        for layers in (1, 4):
+            buf = torch.zeros(n[(a + 1) % 3] * n[(a + 2) % 3] * layers * 8, dtype=torch.float64,
+                              device="cuda")
+            N.check(N.lib.ppmlr_gpu_block_pack_face(blk.h, face, layers,
+                                                    ctypes.c_void_p(buf.data_ptr())))
+            N.check(N.lib.ppmlr_gpu_block_synchronize(blk.h))
+            lo = g if face % 2 == 0 else g + n[a] - layers
+            sl = [slice(g, g + n[2]), slice(g, g + n[1]), slice(g, g + n[0])]
+            sl[2 - a] = slice(lo, lo + layers)
+            order = {0: (0, 1, 2, 3), 1: (2, 0, 1, 3), 2: (1, 2, 0, 3)}[a]
+            want = np.ascontiguousarray(np.transpose(full[tuple(sl)], order)).reshape(-1)
+            assert bits_equal(buf.cpu().numpy(), want), (face, layers)
+            # unpack into the opposite face's ghost shell
+            N.check(N.lib.ppmlr_gpu_block_unpack_face(blk.h, face ^ 1, layers,
+                                                      ctypes.c_void_p(buf.data_ptr())))
+            N.check(N.lib.ppmlr_gpu_block_synchronize(blk.h))
+            after = blk.download()
+            lo2 = g + n[a] if (face ^ 1) % 2 == 1 else g - layers
+            sl2 = list(sl)
+            sl2[2 - a] = slice(lo2, lo2 + layers)
+            assert bits_equal(after[tuple(sl2)], full[tuple(sl)]), (face, layers)
