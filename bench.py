@@ -272,6 +272,34 @@ def bench_single(args):
     # ---- end to end through the public API with host buffers
     e2e = bench_e2e(h, cfg, args, cells) if not args.no_e2e else None
     h.close()
+    del h
+
+    # ---- the other precision mode on the same workload (timing only)
+    other = None
+    if not args.no_secondary:
+        prec2 = "strict" if args.precision == "fast" else "fast"
+        cfg2, _ = make_config(args.config, 1)
+        cfg2.options.precision = prec2
+        h2 = P.Harness(cfg2.specs, cfg2.partition, cfg2.options)
+        if cfg2.ic[0] == "magnetosphere":
+            h2.init_magnetosphere()
+        else:
+            h2.init_with(*cfg2.ic)
+        st2 = torch.cuda.ExternalStream(h2.block(0).stream())
+        h2.run(args.warmup)
+        h2.block(0).synchronize()
+        f0 = torch.cuda.Event(enable_timing=True)
+        f1 = torch.cuda.Event(enable_timing=True)
+        f0.record(st2)
+        h2.run(args.steps)
+        f1.record(st2)
+        f1.synchronize()
+        ms2 = f0.elapsed_time(f1)
+        other = {"precision": prec2, "value": cells * args.steps / (ms2 * 1e-3),
+                 "ms_per_step": ms2 / args.steps,
+                 "note": "strict = bit-identical to the reference CPU build; fast = "
+                         "reciprocal-multiply divisions + FMA, rel. L1 <= 1e-11 / Linf <= 1e-9"}
+        h2.close()
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
@@ -282,7 +310,7 @@ def bench_single(args):
                    "cells_per_gpu": cells, "partition": "x-slab (P,1,1)",
                    "l2": "state (2 x 9 GB ping-pong) >> 126 MB L2; no flush needed"},
         "clocks": clk.summary(), "e2e": e2e, "gpu_launches": int(kernels),
-        "roofline": roofline,
+        "roofline": roofline, "other_precision": other,
     }
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(kind)
@@ -339,7 +367,9 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="blast512")
-    ap.add_argument("--precision", default="strict", choices=["strict", "fast"])
+    ap.add_argument("--precision", default="fast", choices=["strict", "fast"])
+    ap.add_argument("--no-secondary", action="store_true",
+                    help="skip the timing of the other precision mode")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
