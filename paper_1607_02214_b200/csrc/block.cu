@@ -225,9 +225,11 @@ template <class Ops>
 __device__ __forceinline__ void cfl_cands(const double* s, double b0, double b1, double b2,
                                           double d0, double d1, double d2, const KC& c, Ops& o,
                                           double* cand) {
-  cand[0] = o.dv(d0, fabs(s[1]) + fast_speed3<0>(s, b0, b1, b2, c, o));
-  cand[1] = o.dv(d1, fabs(s[2]) + fast_speed3<1>(s, b0, b1, b2, c, o));
-  cand[2] = o.dv(d2, fabs(s[3]) + fast_speed3<2>(s, b0, b1, b2, c, o));
+  double cf[3];
+  fast_speed3_all(s, b0, b1, b2, c, o, cf);
+  cand[0] = o.dv(d0, fabs(s[1]) + cf[0]);
+  cand[1] = o.dv(d1, fabs(s[2]) + cf[1]);
+  cand[2] = o.dv(d2, fabs(s[3]) + cf[2]);
 }
 
 __device__ __forceinline__ bool cfl_cell(const double* s, double b0, double b1, double b2,
@@ -325,6 +327,56 @@ __device__ __forceinline__ void cross3(double ax, double ay, double az, double b
   o[2] = ax * by - ay * bx;
 }
 
+// apply_sources (stepper.cpp:141-200) for one cell from its 7-point
+// stencil: own state s[8] and dipole bo[3]; per axis a the minus/plus
+// neighbours' v and B' (nv[a][side][0..5]) and dipole (nbd[a][side][0..2]);
+// the axis geometry hm, hp, den = (hm*hp)*(hm+hp), rden.  Writes the
+// updated primitive state to q; returns cons_to_prim's code.
+template <class Ops>
+__device__ __forceinline__ int source_update(const double* s, const double* bo,
+                                             const double (*nv)[2][6],
+                                             const double (*nbd)[2][3], const double* hm,
+                                             const double* hp, const double* den,
+                                             const double* rden, const KC& c, double dt,
+                                             Ops& o, double* q) {
+  double gb[3][3], ge[3][3];
+  double e0[3];
+  cross3(s[1], s[2], s[3], bo[0], bo[1], bo[2], e0);
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    double em[3], ep[3];
+    cross3(nv[a][0][0], nv[a][0][1], nv[a][0][2], nbd[a][0][0], nbd[a][0][1], nbd[a][0][2], em);
+    cross3(nv[a][1][0], nv[a][1][1], nv[a][1][2], nbd[a][1][0], nbd[a][1][1], nbd[a][1][2], ep);
+#pragma unroll
+    for (int comp = 0; comp < 3; ++comp) {
+      gb[a][comp] = central_diff(nv[a][0][3 + comp], s[4 + comp], nv[a][1][3 + comp], hm[a], hp[a],
+                                 den[a], rden[a], o);
+      ge[a][comp] = central_diff(em[comp], e0[comp], ep[comp], hm[a], hp[a], den[a], rden[a], o);
+    }
+  }
+  const double cb0 = gb[1][2] - gb[2][1], cb1 = gb[2][0] - gb[0][2], cb2 = gb[0][1] - gb[1][0];
+  const double ce0 = ge[1][2] - ge[2][1], ce1 = ge[2][0] - ge[0][2], ce2 = ge[0][1] - ge[1][0];
+  const double div_b = (gb[0][0] + gb[1][1]) + gb[2][2];
+  double sm[3];
+  cross3(cb0, cb1, cb2, bo[0], bo[1], bo[2], sm);
+  sm[0] = o.div(sm[0], c.c.mu0, c.r_mu0);
+  sm[1] = o.div(sm[1], c.c.mu0, c.r_mu0);
+  sm[2] = o.div(sm[2], c.c.mu0, c.r_mu0);
+  const double si0 = ce0 - s[1] * div_b, si1 = ce1 - s[2] * div_b, si2 = ce2 - s[3] * div_b;
+  const double se = ((s[1] * sm[0] + s[2] * sm[1]) + s[3] * sm[2]) +
+                    o.div((s[4] * ce0 + s[5] * ce1) + s[6] * ce2, c.c.mu0, c.r_mu0);
+  double u[8];
+  prim_to_cons3(s, u, c, o);
+  u[1] = u[1] + sm[0] * dt;
+  u[2] = u[2] + sm[1] * dt;
+  u[3] = u[3] + sm[2] * dt;
+  u[4] = u[4] + si0 * dt;
+  u[5] = u[5] + si1 * dt;
+  u[6] = u[6] + si2 * dt;
+  u[7] = u[7] + dt * se;
+  return cons_to_prim3(u, q, c, o);
+}
+
 struct SrcArgs {
   Planes in, out;
   Lay L;
@@ -347,117 +399,210 @@ struct SrcArgs {
 
 // apply_sources (stepper.cpp:141-200) + restore_frozen_core (:284-286) +
 // the next step's compute_dt (:119-139), one thread per interior cell.
-// FAST: every cell with FastOps; cells whose fast-path guards failed are
-// queued (redo list; on overflow the EXACT pass covers every cell) and left
-// to EXACT, which recomputes them with plain `/` and `sqrt`.
-template <bool DIPOLE, bool EXACT>
-__global__ void __launch_bounds__(256, 2) sources_kernel(const SrcArgs A) {
+// Gathers one cell's 7-point stencil from global memory (EXACT re-run and
+// reference path of the tiled kernel below).
+template <bool DIPOLE>
+__device__ __forceinline__ void gather_stencil(const SrcArgs& A, int i, int j, int k, double* s,
+                                               double* bo, double (*nv)[2][6],
+                                               double (*nbd)[2][3], double* hm, double* hp,
+                                               double* den, double* rden) {
+  const Lay& L = A.L;
+  const long long d = L.idx(i, j, k);
+#pragma unroll
+  for (int f = 0; f < 8; ++f) s[f] = A.in.f[f][d];
+  bo[0] = DIPOLE ? A.bd0[d] : 0.0;
+  bo[1] = DIPOLE ? A.bd1[d] : 0.0;
+  bo[2] = DIPOLE ? A.bd2[d] : 0.0;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const long long st = a == 0 ? 1 : (a == 1 ? L.sy : L.sz);
+    const int lc = (a == 0 ? i : (a == 1 ? j : k)) + kG;
+    hm[a] = (a == 0 ? A.hm0 : (a == 1 ? A.hm1 : A.hm2))[lc];
+    hp[a] = (a == 0 ? A.hp0 : (a == 1 ? A.hp1 : A.hp2))[lc];
+    den[a] = (a == 0 ? A.den0 : (a == 1 ? A.den1 : A.den2))[lc];
+    rden[a] = (a == 0 ? A.rden0 : (a == 1 ? A.rden1 : A.rden2))[lc];
+#pragma unroll
+    for (int side = 0; side < 2; ++side) {
+      const long long dn = side == 0 ? d - st : d + st;
+#pragma unroll
+      for (int f = 0; f < 6; ++f) nv[a][side][f] = A.in.f[1 + f][dn];
+      nbd[a][side][0] = DIPOLE ? A.bd0[dn] : 0.0;
+      nbd[a][side][1] = DIPOLE ? A.bd1[dn] : 0.0;
+      nbd[a][side][2] = DIPOLE ? A.bd2[dn] : 0.0;
+    }
+  }
+}
+
+// Epilogue shared by both source kernels: error key, frozen-core override
+// (restore_frozen_core), store, and the next step's CFL candidates.
+template <bool DIPOLE>
+__device__ __forceinline__ void source_epilogue(const SrcArgs& A, const KC& c, int i, int j,
+                                                int k, long long t, const double* s,
+                                                const double* bo, double* q, int bad,
+                                                unsigned long long step, double& mn) {
+  const Lay& L = A.L;
+  if (bad) {
+    atomicMin(A.ctx.err, err_key(step, kPhaseSources, 0,
+                                 ((unsigned long long)t << 2) |
+                                     (bad == 1 ? kErrDensity : kErrPressure)));
+#pragma unroll
+    for (int f = 0; f < 8; ++f) q[f] = s[f];
+  }
+  if (A.nfrozen > 0) {
+    const int fi = i - A.fl0, fj = j - A.fl1, fk = k - A.fl2;
+    if (fi >= 0 && fi < A.fn0 && fj >= 0 && fj < A.fn1 && fk >= 0 && fk < A.fn2) {
+      const int slot = A.fslot[fi + A.fn0 * (fj + A.fn1 * fk)];
+      if (slot >= 0) {
+#pragma unroll
+        for (int f = 0; f < 8; ++f) q[f] = A.fst[f * A.nfrozen + slot];
+      }
+    }
+  }
+  const long long d = L.idx(i, j, k);
+#pragma unroll
+  for (int f = 0; f < 8; ++f) A.out.f[f][d] = q[f];
+  if (A.fuse_cfl) {
+    int badax = 0;
+    if (!cfl_cell(q, bo[0], bo[1], bo[2], A.dx0[i + kG], A.dx1[j + kG], A.dx2[k + kG], c, mn,
+                  badax))
+      atomicMin(A.ctx.err, err_key(step + 1, kPhaseCfl, 0, ((unsigned long long)t * 3 + badax) << 2));
+  }
+}
+
+// EXACT re-run of the cells queued by the tiled kernel (redo list; on
+// overflow every cell), with plain `/` and `sqrt`.
+template <bool DIPOLE>
+__global__ void __launch_bounds__(256, 2) sources_exact_kernel(const SrcArgs A) {
   const Lay& L = A.L;
   const KC c = make_kc(A.c);
   const long long total = (long long)L.n0 * L.n1 * L.n2;
   double mn = __longlong_as_double(kInfBits);
   const unsigned long long step = *A.ctx.step;
   const double dt = *A.ctx.dt;
-  const bool all = EXACT && *A.redo_count > A.redo_cap;
-  const long long n_items = EXACT ? (all ? total : (long long)*A.redo_count) : total;
+  const bool all = *A.redo_count > A.redo_cap;
+  const long long n_items = all ? total : (long long)*A.redo_count;
   for (long long it = blockIdx.x * (long long)blockDim.x + threadIdx.x; it < n_items;
        it += (long long)gridDim.x * blockDim.x) {
-    const long long t = (EXACT && !all) ? (long long)A.redo_list[it] : it;
+    const long long t = all ? it : (long long)A.redo_list[it];
     const int i = (int)(t % L.n0);
     const int j = (int)((t / L.n0) % L.n1);
     const int k = (int)(t / ((long long)L.n0 * L.n1));
-    const long long d = L.idx(i, j, k);
-    double s[8];
+    double s[8], bo[3], nv[3][2][6], nbd[3][2][3], hm[3], hp[3], den[3], rden[3], q[8];
+    gather_stencil<DIPOLE>(A, i, j, k, s, bo, nv, nbd, hm, hp, den, rden);
+    ExactOps eo;
+    const int bad = source_update(s, bo, nv, nbd, hm, hp, den, rden, c, dt, eo, q);
+    source_epilogue<DIPOLE>(A, c, i, j, k, t, s, bo, q, bad, step, mn);
+  }
+  if (A.fuse_cfl) block_min_commit(mn, A.ctx.min);
+}
+
+// apply_sources (stepper.cpp:141-200) + restore_frozen_core (:284-286) +
+// the next step's compute_dt (:119-139), 2.5-D blocked: a CTA owns a 32x8
+// (x, y) tile and marches through a z chunk, keeping the planes z-1, z, z+1
+// (v, B' and the dipole, with a one-cell x/y halo) in a shared-memory ring,
+// so every stencil input is fetched from HBM once.  FastOps; cells whose
+// fast-path guards fail are queued for sources_exact_kernel.
+constexpr int kSrcTX = 32, kSrcTY = 8, kSrcHX = kSrcTX + 2, kSrcHY = kSrcTY + 2;
+
+template <bool DIPOLE>
+__global__ void __launch_bounds__(kSrcTX * kSrcTY, 2) sources_tiled_kernel(const SrcArgs A,
+                                                                            int zchunk) {
+  constexpr int NF = DIPOLE ? 9 : 6;
+  constexpr int PL = kSrcHX * kSrcHY;  // cells per plane (incl. halo)
+  extern __shared__ double ring[];     // [3][NF][PL]
+  const Lay& L = A.L;
+  const KC c = make_kc(A.c);
+  const int tx = threadIdx.x % kSrcTX, ty = threadIdx.x / kSrcTX;
+  const int x0 = blockIdx.x * kSrcTX, y0 = blockIdx.y * kSrcTY;
+  const int z0 = blockIdx.z * zchunk, z1 = min(L.n2, z0 + zchunk);
+  const int i = x0 + tx, j = y0 + ty;
+  const bool in_xy = i < L.n0 && j < L.n1;
+  const unsigned long long step = *A.ctx.step;
+  const double dt = *A.ctx.dt;
+  double mn = __longlong_as_double(kInfBits);
+
+  auto load_plane = [&](int z, int slot) {
+    double* dstp = ring + (size_t)slot * NF * PL;
+    for (int c2 = threadIdx.x; c2 < PL; c2 += blockDim.x) {
+      const int xx = c2 % kSrcHX, yy = c2 / kSrcHX;
+      const bool corner = (xx == 0 || xx == kSrcHX - 1) && (yy == 0 || yy == kSrcHY - 1);
+      if (corner) continue;
+      const long long d = L.idx(x0 - 1 + xx, y0 - 1 + yy, z);
 #pragma unroll
-    for (int f = 0; f < 8; ++f) s[f] = A.in.f[f][d];
-    const double b0 = DIPOLE ? A.bd0[d] : 0.0, b1 = DIPOLE ? A.bd1[d] : 0.0,
-                 b2 = DIPOLE ? A.bd2[d] : 0.0;
-    double q[8];
-    int bad = 0;
-    auto compute = [&](auto& o) {
-    double gb[3][3], ge[3][3];
-    double e0[3];
-    cross3(s[1], s[2], s[3], b0, b1, b2, e0);
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      const long long st = a == 0 ? 1 : (a == 1 ? L.sy : L.sz);
-      const long long dm = d - st, dp = d + st;
-      const int lc = (a == 0 ? i : (a == 1 ? j : k)) + kG;
-      const double hm = (a == 0 ? A.hm0 : (a == 1 ? A.hm1 : A.hm2))[lc];
-      const double hp = (a == 0 ? A.hp0 : (a == 1 ? A.hp1 : A.hp2))[lc];
-      const double den = (a == 0 ? A.den0 : (a == 1 ? A.den1 : A.den2))[lc];
-      const double rden = (a == 0 ? A.rden0 : (a == 1 ? A.rden1 : A.rden2))[lc];
-      double em[3], ep[3];
-      cross3(A.in.f[1][dm], A.in.f[2][dm], A.in.f[3][dm], DIPOLE ? A.bd0[dm] : 0.0,
-             DIPOLE ? A.bd1[dm] : 0.0, DIPOLE ? A.bd2[dm] : 0.0, em);
-      cross3(A.in.f[1][dp], A.in.f[2][dp], A.in.f[3][dp], DIPOLE ? A.bd0[dp] : 0.0,
-             DIPOLE ? A.bd1[dp] : 0.0, DIPOLE ? A.bd2[dp] : 0.0, ep);
-#pragma unroll
-      for (int comp = 0; comp < 3; ++comp) {
-        gb[a][comp] =
-            central_diff(A.in.f[4 + comp][dm], s[4 + comp], A.in.f[4 + comp][dp], hm, hp, den, rden, o);
-        ge[a][comp] = central_diff(em[comp], e0[comp], ep[comp], hm, hp, den, rden, o);
+      for (int f = 0; f < 6; ++f) dstp[f * PL + c2] = A.in.f[1 + f][d];
+      if (DIPOLE) {
+        dstp[6 * PL + c2] = A.bd0[d];
+        dstp[7 * PL + c2] = A.bd1[d];
+        dstp[8 * PL + c2] = A.bd2[d];
       }
     }
-    const double cb0 = gb[1][2] - gb[2][1], cb1 = gb[2][0] - gb[0][2], cb2 = gb[0][1] - gb[1][0];
-    const double ce0 = ge[1][2] - ge[2][1], ce1 = ge[2][0] - ge[0][2], ce2 = ge[0][1] - ge[1][0];
-    const double div_b = (gb[0][0] + gb[1][1]) + gb[2][2];
-    double sm[3];
-    cross3(cb0, cb1, cb2, b0, b1, b2, sm);
-    sm[0] = o.div(sm[0], c.c.mu0, c.r_mu0);
-    sm[1] = o.div(sm[1], c.c.mu0, c.r_mu0);
-    sm[2] = o.div(sm[2], c.c.mu0, c.r_mu0);
-    const double si0 = ce0 - s[1] * div_b, si1 = ce1 - s[2] * div_b, si2 = ce2 - s[3] * div_b;
-    const double se = ((s[1] * sm[0] + s[2] * sm[1]) + s[3] * sm[2]) +
-                      o.div((s[4] * ce0 + s[5] * ce1) + s[6] * ce2, c.c.mu0, c.r_mu0);
-    double u[8];
-    prim_to_cons3(s, u, c, o);
-    u[1] = u[1] + sm[0] * dt;
-    u[2] = u[2] + sm[1] * dt;
-    u[3] = u[3] + sm[2] * dt;
-    u[4] = u[4] + si0 * dt;
-    u[5] = u[5] + si1 * dt;
-    u[6] = u[6] + si2 * dt;
-    u[7] = u[7] + dt * se;
-    bad = cons_to_prim3(u, q, c, o);
-    };
-    if (EXACT) {
-      ExactOps eo;
-      compute(eo);
-    } else {
+  };
+  load_plane(z0 - 1, (z0 + 2) % 3);
+  load_plane(z0, z0 % 3);
+  // per-thread constant geometry along x and y
+  double hm[3], hp[3], den[3], rden[3];
+  if (in_xy) {
+    hm[0] = A.hm0[i + kG];
+    hp[0] = A.hp0[i + kG];
+    den[0] = A.den0[i + kG];
+    rden[0] = A.rden0[i + kG];
+    hm[1] = A.hm1[j + kG];
+    hp[1] = A.hp1[j + kG];
+    den[1] = A.den1[j + kG];
+    rden[1] = A.rden1[j + kG];
+  }
+  const int cc = (ty + 1) * kSrcHX + (tx + 1);  // this cell in a plane
+  for (int k = z0; k < z1; ++k) {
+    load_plane(k + 1, (k + 1) % 3);
+    __syncthreads();
+    if (in_xy) {
+      const double* pm = ring + (size_t)((k + 2) % 3) * NF * PL;
+      const double* p0 = ring + (size_t)(k % 3) * NF * PL;
+      const double* pp = ring + (size_t)((k + 1) % 3) * NF * PL;
+      const long long d = L.idx(i, j, k);
+      double s[8], bo[3], nv[3][2][6], nbd[3][2][3], q[8];
+      s[0] = A.in.f[0][d];
+      s[7] = A.in.f[7][d];
+#pragma unroll
+      for (int f = 0; f < 6; ++f) s[1 + f] = p0[f * PL + cc];
+#pragma unroll
+      for (int f = 0; f < 3; ++f) bo[f] = DIPOLE ? p0[(6 + f) * PL + cc] : 0.0;
+      const int nb_off[2][2] = {{cc - 1, cc + 1}, {cc - kSrcHX, cc + kSrcHX}};
+#pragma unroll
+      for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int side = 0; side < 2; ++side) {
+#pragma unroll
+          for (int f = 0; f < 6; ++f) nv[a][side][f] = p0[f * PL + nb_off[a][side]];
+#pragma unroll
+          for (int f = 0; f < 3; ++f)
+            nbd[a][side][f] = DIPOLE ? p0[(6 + f) * PL + nb_off[a][side]] : 0.0;
+        }
+#pragma unroll
+      for (int f = 0; f < 6; ++f) {
+        nv[2][0][f] = pm[f * PL + cc];
+        nv[2][1][f] = pp[f * PL + cc];
+      }
+#pragma unroll
+      for (int f = 0; f < 3; ++f) {
+        nbd[2][0][f] = DIPOLE ? pm[(6 + f) * PL + cc] : 0.0;
+        nbd[2][1][f] = DIPOLE ? pp[(6 + f) * PL + cc] : 0.0;
+      }
+      hm[2] = A.hm2[k + kG];
+      hp[2] = A.hp2[k + kG];
+      den[2] = A.den2[k + kG];
+      rden[2] = A.rden2[k + kG];
       FastOps fo;
-      compute(fo);
+      const int bad = source_update(s, bo, nv, nbd, hm, hp, den, rden, c, dt, fo, q);
+      const long long t = (long long)i + (long long)L.n0 * ((long long)j + (long long)L.n1 * k);
       if (fo.bad) {
         const unsigned slot = atomicAdd(A.redo_count, 1u);
         if (slot < A.redo_cap) A.redo_list[slot] = (unsigned)t;
-        continue;
+      } else {
+        source_epilogue<DIPOLE>(A, c, i, j, k, t, s, bo, q, bad, step, mn);
       }
     }
-    if (bad) {
-      atomicMin(A.ctx.err, err_key(step, kPhaseSources, 0,
-                                   ((unsigned long long)t << 2) |
-                                       (bad == 1 ? kErrDensity : kErrPressure)));
-#pragma unroll
-      for (int f = 0; f < 8; ++f) q[f] = s[f];
-    }
-    // frozen inner core overrides the update (restore_frozen_core)
-    if (A.nfrozen > 0) {
-      const int fi = i - A.fl0, fj = j - A.fl1, fk = k - A.fl2;
-      if (fi >= 0 && fi < A.fn0 && fj >= 0 && fj < A.fn1 && fk >= 0 && fk < A.fn2) {
-        const int slot = A.fslot[fi + A.fn0 * (fj + A.fn1 * fk)];
-        if (slot >= 0) {
-#pragma unroll
-          for (int f = 0; f < 8; ++f) q[f] = A.fst[f * A.nfrozen + slot];
-        }
-      }
-    }
-#pragma unroll
-    for (int f = 0; f < 8; ++f) A.out.f[f][d] = q[f];
-    if (A.fuse_cfl) {
-      int badax = 0;
-      if (!cfl_cell(q, b0, b1, b2, A.dx0[i + kG], A.dx1[j + kG], A.dx2[k + kG], c, mn, badax))
-        atomicMin(A.ctx.err, err_key(step + 1, kPhaseCfl, 0, ((unsigned long long)t * 3 + badax) << 2));
-    }
+    __syncthreads();
   }
   if (A.fuse_cfl) block_min_commit(mn, A.ctx.min);
 }
@@ -809,18 +954,25 @@ int launch_sources(ppmlr_gpu_block* b, int fuse_cfl) {
   A.redo_count = b->d_redo;
   A.redo_list = b->d_redo + 1;
   A.redo_cap = b->redo_cap;
-  const long long work = (long long)b->n[0] * b->n[1] * b->n[2];
   CK(cudaMemsetAsync(b->d_redo, 0, sizeof(unsigned), b->stream));
+  const int zchunk = std::min(b->n[2], 32);
+  const dim3 grid((b->n[0] + kSrcTX - 1) / kSrcTX, (b->n[1] + kSrcTY - 1) / kSrcTY,
+                  (b->n[2] + zchunk - 1) / zchunk);
+  const int nf = b->with_dipole ? 9 : 6;
+  const size_t smem = sizeof(double) * 3 * nf * kSrcHX * kSrcHY;
   if (b->with_dipole) {
-    sources_kernel<true, false><<<grid_for(work), 256, 0, b->stream>>>(A);
-    sources_kernel<true, true><<<148, 256, 0, b->stream>>>(A);
+    CK(cudaFuncSetAttribute(sources_tiled_kernel<true>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    sources_tiled_kernel<true><<<grid, kSrcTX * kSrcTY, smem, b->stream>>>(A, zchunk);
+    sources_exact_kernel<true><<<148, 256, 0, b->stream>>>(A);
   } else {
-    sources_kernel<false, false><<<grid_for(work), 256, 0, b->stream>>>(A);
-    sources_kernel<false, true><<<148, 256, 0, b->stream>>>(A);
+    CK(cudaFuncSetAttribute(sources_tiled_kernel<false>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    sources_tiled_kernel<false><<<grid, kSrcTX * kSrcTY, smem, b->stream>>>(A, zchunk);
+    sources_exact_kernel<false><<<148, 256, 0, b->stream>>>(A);
   }
   CK(cudaGetLastError());
-  b->kernel_launches += 1;
-  b->kernel_launches += 1;
+  b->kernel_launches += 2;
   b->cur ^= 1;
   return 0;
 }

@@ -59,6 +59,30 @@ __device__ __forceinline__ double fast_speed3(const double* s, double bdx, doubl
   return o.sq(0.5 * (sum + disc));
 }
 
+// fast_speed3 for the three directions at once (compute_dt,
+// stepper.cpp:128-137): a2, ca2, sum, sum*sum and 4*a2 do not depend on the
+// direction, so they are evaluated once (identical operands -> identical
+// bits).
+template <class Ops>
+__device__ __forceinline__ void fast_speed3_all(const double* s, double bdx, double bdy,
+                                                double bdz, const KC& k, Ops& o, double* cf) {
+  const double b0 = s[4] + bdx, b1 = s[5] + bdy, b2 = s[6] + bdz;
+  const double mr = k.c.mu0 * s[0];
+  const double r_mr = o.rcp(mr);
+  const double a2 = o.dv(k.c.gamma * s[7], s[0]);
+  const double ca2 = o.div((b0 * b0 + b1 * b1) + b2 * b2, mr, r_mr);
+  const double sum = a2 + ca2;
+  const double ss = sum * sum;
+  const double a4 = 4.0 * a2;
+  const double bb[3] = {b0, b1, b2};
+#pragma unroll
+  for (int dir = 0; dir < 3; ++dir) {
+    const double can2 = o.div(bb[dir] * bb[dir], mr, r_mr);
+    const double disc = o.sq(smax(0.0, ss - a4 * can2));
+    cf[dir] = o.sq(0.5 * (sum + disc));
+  }
+}
+
 // ppm1d.cpp:29-37 fast_speed_strip: |b|^2 in strip order.
 template <class Ops>
 __device__ __forceinline__ double fast_speed_strip(double rho, double p, double btn,
