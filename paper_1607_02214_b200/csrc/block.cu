@@ -804,7 +804,7 @@ void choose_sweep_tiles(ppmlr_gpu_block* b) {
   // Segments of kSweepTL - 8 = 64 cells (compile-time tile) when the axis is a
   // multiple of 64 or long enough that a partial last segment costs little;
   // otherwise balanced segments of at most Lmax cells (runtime tile).
-  b->sweep_version = env_int("PPMLR_SWEEP_V", 2);
+  b->sweep_version = env_int("PPMLR_SWEEP_V", 3);
   // v2 runs one cell per thread: a tile is at most 512 cells (L <= 120)
   const int Lmax = std::min(env_int("PPMLR_SWEEP_LMAX", 64), b->sweep_version == 1 ? 1 << 20 : 120);
   const int ipt = b->sweep_version == 1 ? env_int("PPMLR_SWEEP_IPT", 1) : 1;  // v2: 1 cell/thread
@@ -866,7 +866,7 @@ int launch_sweep(ppmlr_gpu_block* b, int axis, int phase) {
   A.redo_count = b->d_redo;
   A.redo_list = b->d_redo + 1;
   const int T = 4 * (A.L + 8);
-  const int slots = (b->sweep_version == 1 ? 33 : 25) + (b->with_dipole ? 3 : 0);
+  const int slots = (b->sweep_version == 2 ? 25 : 33) + (b->with_dipole ? 3 : 0);
   const size_t smem = sizeof(double) * (size_t)T * slots;
   // The sweep writes only the interior of the output buffer; its ghost
   // shells stay stale until the next fill (every reader fills first).

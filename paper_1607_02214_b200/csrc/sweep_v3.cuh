@@ -1,0 +1,323 @@
+// Directional PPMLR sweep, v3 tile schedule (fused primitive reconstruction,
+// conserved slopes once per cell, 5 barriers).
+//
+// Same contract and bit-exactness as sweep.cuh (v1).  One thread per cell:
+//
+//   P0  load; strip-frame prim, cons, c_f                  -> PRIM, CONS, CF
+//   P3  per zone: prim parabola from the 5-point window
+//       PRIM[s-2..s+2] -> traced L/R                        -> SA:=L, SB:=R
+//   P4  per edge: Riemann solve                            -> CF:=u*, SA:=flux
+//   P7  per zone: Lagrangian update + checks                -> SB:=lag
+//       and the conserved slope of the cell                 -> PRIM:=dm
+//   P8  per moving edge: the upwind zone's conserved interface values
+//       from CONS and dm, limiter, remap sliver             -> SA:=sliver
+//   P9  per zone: remap, cons_to_prim, store
+//
+// 33 shared slots per cell (+3 with the dipole), 5 barriers.
+#pragma once
+#include "sweep_v2.cuh"
+
+namespace ppmlr_b200 {
+namespace PPMLR_KNS {
+
+template <int AXIS, bool DIPOLE, int NP, int TLC, class Ops>
+__device__ __forceinline__ bool sweep_tile_v3(const SweepArgs& A, const int bid, double* smem,
+                                              unsigned long long* s_err) {
+  bool tbad = false;
+  const int TL = TLC > 0 ? TLC : A.L + 8;
+  const int T = NP * TL;
+  double* PRIM = smem;
+  double* CONS = smem + 8 * T;
+  double* CF = smem + 16 * T;
+  double* SA = smem + 17 * T;
+  double* SB = smem + 25 * T;
+  double* BD = smem + 33 * T;
+  const int SS = AXIS == 0 ? 1 : NP;
+
+  const int seg = bid % A.nseg;
+  const int rest = bid / A.nseg;
+  const int grp = rest % A.ngroups;
+  const int oc = rest / A.ngroups;
+  const int nn = A.n + 8;
+  const int seg0 = seg * A.L;
+  const int TLv = min(TL, nn - seg0);
+  const bool final_seg = seg == A.nseg - 1;
+  const int zmax = final_seg ? TLv - 2 : TL - 3;
+  const int g0 = grp * NP;
+  const int npv = min(NP, A.ng - g0);
+  const double dt = *A.dt;
+  const Consts& c = A.c;
+  const KC k = make_kc(c);
+  const long long base = (long long)(g0 + 4) * A.stride_g + (long long)(oc + 4) * A.stride_o +
+                         (long long)seg0 * A.stride_a;
+  // one cell per thread (the launcher guarantees blockDim.x >= T)
+  const int ci = threadIdx.x;
+  int s, p;
+  if (AXIS == 0) {
+    p = ci / TL;
+    s = ci - p * TL;
+  } else {
+    s = ci / NP;
+    p = ci - s * NP;
+  }
+  const bool live = ci < T && p < npv;
+  const int q = seg0 + s;
+  auto pencil_index = [&]() -> unsigned long long {
+    const int gcoord = g0 + p;
+    const int t1 = AXIS == 1 ? oc : gcoord;
+    const int t2 = AXIS == 1 ? gcoord : oc;
+    return (unsigned long long)t1 + (unsigned long long)A.nb * (unsigned long long)t2;
+  };
+  constexpr int a = AXIS, b = (AXIS + 1) % 3, d = (AXIS + 2) % 3;
+
+  // ---- P0 ---------------------------------------------------------------
+  if (live && s < TLv) {
+    const long long off = base + (long long)p * A.stride_g + (long long)s * A.stride_a;
+    double qv[8];
+#pragma unroll
+    for (int f = 0; f < 8; ++f) qv[f] = __ldg(A.src[f] + off);
+    double b0 = 0.0, b1 = 0.0, b2 = 0.0;
+    if (DIPOLE) {
+      b0 = __ldg(A.bd[0] + off);
+      b1 = __ldg(A.bd[1] + off);
+      b2 = __ldg(A.bd[2] + off);
+      BD[0 * T + ci] = AXIS == 0 ? b0 : (AXIS == 1 ? b1 : b2);
+      BD[1 * T + ci] = AXIS == 0 ? b1 : (AXIS == 1 ? b2 : b0);
+      BD[2 * T + ci] = AXIS == 0 ? b2 : (AXIS == 1 ? b0 : b1);
+    }
+    double w[8];
+    w[kRho] = qv[0];
+    w[kUn] = qv[1 + a];
+    w[kUt1] = qv[1 + b];
+    w[kUt2] = qv[1 + d];
+    w[kBn] = qv[4 + a];
+    w[kBt1] = qv[4 + b];
+    w[kBt2] = qv[4 + d];
+    w[kPE] = qv[7];
+    Ops o;
+    const double cf = fast_speed3<AXIS>(qv, b0, b1, b2, k, o);
+    const double e = strip_energy(w, k, o);
+    tbad |= o.bad;
+    CF[ci] = cf;
+#pragma unroll
+    for (int v = 0; v < 8; ++v) PRIM[v * T + ci] = w[v];
+    CONS[kRho * T + ci] = w[kRho];
+    CONS[kUn * T + ci] = w[kRho] * w[kUn];
+    CONS[kUt1 * T + ci] = w[kRho] * w[kUt1];
+    CONS[kUt2 * T + ci] = w[kRho] * w[kUt2];
+    CONS[kBn * T + ci] = w[kBn];
+    CONS[kBt1 * T + ci] = w[kBt1];
+    CONS[kBt2 * T + ci] = w[kBt2];
+    CONS[kPE * T + ci] = e;
+  }
+  __syncthreads();
+
+  // ---- P3: prim parabolas -> traced states (zones [2, zmax]) ------------
+  if (live && s >= 2 && s <= zmax) {
+    const bool flat = q >= nn - 2;  // q >= 2 always here
+    double sc[9], e0[5], e1[5];
+    if (!flat) {
+#pragma unroll
+      for (int j = 0; j < 9; ++j) sc[j] = __ldg(A.slope + 3 * (q - 1) + j);
+#pragma unroll
+      for (int j = 0; j < 5; ++j) {
+        e0[j] = __ldg(A.qfc + 5 * q + j);
+        e1[j] = __ldg(A.qfc + 5 * (q + 1) + j);
+      }
+    }
+    Ops o;
+    const double sigma =
+        sclamp(o.div(CF[ci] * dt, __ldg(A.dx + q), __ldg(A.rdx + q)), 0.0, 1.0);
+    const double hs = 0.5 * sigma;
+    const double tw = tw_of(sigma, k, o);
+    double L[8], R[8];
+#pragma unroll
+    for (int v = 0; v < 8; ++v) {
+      const double* pv = PRIM + v * T + ci;
+      const double av = pv[0];
+      double al = av, ar = av, six = 0.0;
+      if (!flat) {
+        auto win = [&](int j) { return pv[j * SS]; };
+        zone_parabola(win, sc, e0, e1, k, o, al, ar, six);
+      }
+      L[v] = avg_left(al, ar, six, hs, tw);
+      R[v] = avg_right(al, ar, six, hs, tw);
+    }
+    tbad |= o.bad;
+    const bool badL = !(L[kRho] > 0.0) || !(L[kPE] > 0.0);
+    const bool badR = !(R[kRho] > 0.0) || !(R[kPE] > 0.0);
+#pragma unroll
+    for (int v = 0; v < 8; ++v) {
+      const double own = PRIM[v * T + ci];
+      SA[v * T + ci] = badL ? own : L[v];
+      SB[v * T + ci] = badR ? own : R[v];
+    }
+  }
+  __syncthreads();
+
+  // ---- P4: edge solve at m in [3, zmax] ---------------------------------
+  if (live && s >= 3 && s <= zmax) {
+    double f[8], bl[3] = {0.0, 0.0, 0.0}, br[3] = {0.0, 0.0, 0.0};
+    const SmemVec ql{SB + ci - SS, T}, qr{SA + ci, T};
+    if (DIPOLE) {
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        bl[j] = BD[j * T + ci - SS];
+        br[j] = BD[j * T + ci];
+      }
+    }
+    Ops o;
+    const double us = solve_edge(ql, qr, bl, br, k, f, o);
+    tbad |= o.bad;
+    CF[ci] = us;
+#pragma unroll
+    for (int v = 0; v < 8; ++v) SA[v * T + ci] = f[v];
+  }
+  __syncthreads();
+
+  // ---- P7: Lagrangian update of zones [3, zmax-1] -> SB; cons slopes -> PRIM
+  if (live && s >= 3 && s <= zmax - 1) {
+    const double dx0 = __ldg(A.dx + q);
+    const double dxp = dx0 + dt * (CF[ci + SS] - CF[ci]);
+    if (!(dxp > 0.0)) {
+      atomicMin(s_err, err_key(*A.step, A.phase, AXIS,
+                               (pencil_index() << 20) | ((unsigned long long)q << 2) |
+                                   kErrStepRejected));
+    } else {
+      double u[8];
+      Ops o;
+      const double r_dxp = o.rcp(dxp);
+      const double shrink = o.div(dx0, dxp, r_dxp);
+#pragma unroll
+      for (int v = 0; v < 8; ++v)
+        u[v] = CONS[v * T + ci] * shrink -
+               o.div(dt * (SA[v * T + ci + SS] - SA[v * T + ci]), dxp, r_dxp);
+      const double internal =
+          (u[kPE] - o.dv(0.5 * ((u[kUn] * u[kUn] + u[kUt1] * u[kUt1]) + u[kUt2] * u[kUt2]),
+                         u[kRho])) -
+          o.div((u[kBn] * u[kBn] + u[kBt1] * u[kBt1]) + u[kBt2] * u[kBt2], c.two_mu0,
+                k.r_two_mu0);
+      tbad |= o.bad;
+#pragma unroll
+      for (int v = 0; v < 8; ++v) SB[v * T + ci] = u[v];
+      if (c.pressure_floor <= 0.0 && (!(u[kRho] > 0.0) || !(internal > 0.0)))
+        atomicMin(s_err, err_key(*A.step, A.phase, AXIS,
+                                 (pencil_index() << 20) | ((unsigned long long)q << 2) |
+                                     kErrLagUnphysical));
+    }
+  }
+  if (live && s >= 2 && s <= TLv - 3) {
+    const double* gc = A.slope + 3 * q;
+    const double c0 = __ldg(gc), cA = __ldg(gc + 1), cB = __ldg(gc + 2);
+#pragma unroll
+    for (int v = 0; v < 8; ++v) {
+      const double* cv = CONS + v * T + ci;
+      PRIM[v * T + ci] = limited_slope(cv[-SS], cv[0], cv[SS], c0, cA, cB);
+    }
+  }
+  __syncthreads();
+
+  // ---- P8: slivers at edges [4, TLv-4] (moving edges only) -> SA --------
+  if (live && s >= 4 && s <= TLv - 4) {
+    const double delta = CF[ci] * dt;
+    double sl[8];
+#pragma unroll
+    for (int v = 0; v < 8; ++v) sl[v] = 0.0;
+    if (delta != 0.0) {
+      const bool right = delta > 0.0;
+      const int kc = right ? ci - SS : ci;  // upwind zone
+      const int kq = right ? q - 1 : q;
+      const double width = __ldg(A.dx + kq) + dt * (CF[kc + SS] - CF[kc]);
+      double e0[5], e1[5];
+#pragma unroll
+      for (int j = 0; j < 5; ++j) {
+        e0[j] = __ldg(A.qfc + 5 * kq + j);
+        e1[j] = __ldg(A.qfc + 5 * (kq + 1) + j);
+      }
+      Ops o;
+      const double sigma = o.dv(right ? delta : -delta, width);
+      const double hs = 0.5 * sigma;
+      const double tw = tw_of(sigma, k, o);
+#pragma unroll
+      for (int v = 0; v < 8; ++v) {
+        const double* cv = CONS + v * T + kc;
+        const double* dm = PRIM + v * T + kc;
+        double al = interface_value(cv[-SS], cv[0], dm[-SS], dm[0], e0);
+        double ar = interface_value(cv[0], cv[SS], dm[0], dm[SS], e1);
+        double six;
+        limit_parabola(al, ar, cv[0], six, k, o);
+        const double mean =
+            right ? avg_right(al, ar, six, hs, tw) : avg_left(al, ar, six, hs, tw);
+        sl[v] = delta * (mean + (SB[v * T + kc] - cv[0]));
+      }
+      tbad |= o.bad;
+    }
+#pragma unroll
+    for (int v = 0; v < 8; ++v) SA[v * T + ci] = sl[v];
+  }
+  __syncthreads();
+
+  // ---- P9: remap, cons_to_prim, store (zones [4, TLv-5]) ----------------
+  if (live && s >= 4 && s <= TLv - 5) {
+    const double dxe = __ldg(A.dx + q);
+    const double r_dxe = __ldg(A.rdx + q);
+    const double width = dxe + dt * (CF[ci + SS] - CF[ci]);
+    double out[8], u[8], cs[8];
+    Ops o;
+    const double scale = o.div(width, dxe, r_dxe);
+#pragma unroll
+    for (int v = 0; v < 8; ++v)
+      u[v] = SB[v * T + ci] * scale + o.div(SA[v * T + ci] - SA[v * T + ci + SS], dxe, r_dxe);
+    cs[0] = u[kRho];
+    cs[1 + a] = u[kUn];
+    cs[1 + b] = u[kUt1];
+    cs[1 + d] = u[kUt2];
+    cs[4 + a] = u[kBn];
+    cs[4 + b] = u[kBt1];
+    cs[4 + d] = u[kBt2];
+    cs[7] = u[kPE];
+    const int bad = cons_to_prim3(cs, out, k, o);
+    tbad |= o.bad;
+    if (bad) {
+      atomicMin(s_err, err_key(*A.step, A.phase, AXIS,
+                               (pencil_index() << 20) | (1ull << 19) |
+                                   ((unsigned long long)(q - 4) << 2) |
+                                   (bad == 1 ? kErrDensity : kErrPressure)));
+    } else {
+      const long long off = base + (long long)p * A.stride_g + (long long)s * A.stride_a;
+#pragma unroll
+      for (int f = 0; f < 8; ++f) A.dst[f][off] = out[f];
+    }
+  }
+  return tbad;
+}
+
+template <int AXIS, bool DIPOLE, int NP, int TLC, bool EXACT>
+__global__ void __launch_bounds__(TLC > 0 ? NP * TLC : 512, TLC > 0 ? 2 : 1)
+    sweep_kernel_v3(const SweepArgs A) {
+  extern __shared__ double smem[];
+  __shared__ unsigned long long s_err;
+  if (EXACT) {
+    const unsigned n = *A.redo_count;
+    for (unsigned i = blockIdx.x; i < n; i += gridDim.x) {
+      if (threadIdx.x == 0) s_err = kNoError;
+      __syncthreads();
+      sweep_tile_v3<AXIS, DIPOLE, NP, TLC, ExactOps>(A, (int)A.redo_list[i], smem, &s_err);
+      __syncthreads();
+      if (threadIdx.x == 0 && s_err != kNoError) atomicMin(A.err, s_err);
+      __syncthreads();
+    }
+    return;
+  }
+  if (threadIdx.x == 0) s_err = kNoError;
+  __syncthreads();
+  const bool bad = sweep_tile_v3<AXIS, DIPOLE, NP, TLC, MainOps>(A, blockIdx.x, smem, &s_err);
+  if (__syncthreads_or(bad)) {
+    if (threadIdx.x == 0) A.redo_list[atomicAdd(A.redo_count, 1u)] = blockIdx.x;
+  } else if (threadIdx.x == 0 && s_err != kNoError) {
+    atomicMin(A.err, s_err);
+  }
+}
+
+}  // namespace PPMLR_KNS
+}  // namespace ppmlr_b200
