@@ -866,7 +866,8 @@ int launch_sweep(ppmlr_gpu_block* b, int axis, int phase) {
   A.redo_count = b->d_redo;
   A.redo_list = b->d_redo + 1;
   const int T = 4 * (A.L + 8);
-  const int slots = (b->sweep_version == 2 ? 25 : 33) + (b->with_dipole ? 3 : 0);
+  const int v = b->sweep_version;
+  const int slots = (v == 2 || v == 4 || v == 5 || v == 6 ? 25 : 33) + (b->with_dipole ? 3 : 0);
   const size_t smem = sizeof(double) * (size_t)T * slots;
   // The sweep writes only the interior of the output buffer; its ghost
   // shells stay stale until the next fill (every reader fills first).

@@ -1,4 +1,5 @@
-// Directional PPMLR sweep, v2 tile schedule (fused reconstructions).
+// Directional PPMLR sweep, v5 tile schedule: v2 with the primitive slopes
+// computed once per cell (P1) instead of three times per zone.
 //
 // Same contract and bit-exactness as sweep.cuh (v1); the difference is the
 // phase structure.  One thread per cell of a NP x TL tile (TL = L + 8):
@@ -22,28 +23,24 @@
 // interface values per zone instead of 1 and 1): identical operands, hence
 // identical results.
 #pragma once
-#include "sweep.cuh"
+#include "sweep_v2.cuh"
 
 namespace ppmlr_b200 {
 namespace PPMLR_KNS {
 
-// The limited parabola of zone (tile row s) from the 5-point window of one
-// variable: reconstruct() (ppm1d.cpp:200-247) restricted to one zone.
-template <class W, class Ops>
-__device__ __forceinline__ void zone_parabola(const W& q, const double* sc, const double* e0,
-                                              const double* e1, const KC& k, Ops& o,
-                                              double& al, double& ar, double& six) {
-  // q(-2..2); sc: slope coefficients at positions q-1, q, q+1 (3 each)
-  const double dmm = limited_slope(q(-2), q(-1), q(0), sc[0], sc[1], sc[2]);
-  const double dm0 = limited_slope(q(-1), q(0), q(1), sc[3], sc[4], sc[5]);
-  const double dmp = limited_slope(q(0), q(1), q(2), sc[6], sc[7], sc[8]);
-  al = interface_value(q(-1), q(0), dmm, dm0, e0);
-  ar = interface_value(q(0), q(1), dm0, dmp, e1);
+// Limited parabola of a zone from its 3-point window and the stored slopes
+// of the window (reconstruct(), ppm1d.cpp:200-247, restricted to one zone).
+template <class W, class D, class Ops>
+__device__ __forceinline__ void zone_parabola_dm(const W& q, const D& dm, const double* e0,
+                                                 const double* e1, const KC& k, Ops& o,
+                                                 double& al, double& ar, double& six) {
+  al = interface_value(q(-1), q(0), dm(-1), dm(0), e0);
+  ar = interface_value(q(0), q(1), dm(0), dm(1), e1);
   limit_parabola(al, ar, q(0), six, k, o);
 }
 
 template <int AXIS, bool DIPOLE, int NP, int TLC, class Ops>
-__device__ __forceinline__ bool sweep_tile_v2(const SweepArgs& A, const int bid, double* smem,
+__device__ __forceinline__ bool sweep_tile_v5(const SweepArgs& A, const int bid, double* smem,
                                               unsigned long long* s_err) {
   bool tbad = false;
   const int TL = TLC > 0 ? TLC : A.L + 8;
@@ -133,15 +130,25 @@ __device__ __forceinline__ bool sweep_tile_v2(const SweepArgs& A, const int bid,
   }
   __syncthreads();
 
+  // ---- P1: primitive slopes at s in [1, TLv-2] -> SA ---------------------
+  if (live && s >= 1 && s <= TLv - 2) {
+    const double* gc = A.slope + 3 * q;
+    const double c0 = __ldg(gc), cA = __ldg(gc + 1), cB = __ldg(gc + 2);
+#pragma unroll
+    for (int v = 0; v < 8; ++v) {
+      const double* pv = PRIM + v * T + ci;
+      SA[v * T + ci] = limited_slope(pv[-SS], pv[0], pv[SS], c0, cA, cB);
+    }
+  }
+  __syncthreads();
+
   // ---- P3: prim parabolas -> traced states (zones [2, zmax]) ------------
   double L[8], R[8];
   const bool z3 = live && s >= 2 && s <= zmax;
   if (z3) {
     const bool flat = q >= nn - 2;  // q >= 2 always here
-    double sc[9], e0[5], e1[5];
+    double e0[5], e1[5];
     if (!flat) {
-#pragma unroll
-      for (int j = 0; j < 9; ++j) sc[j] = __ldg(A.slope + 3 * (q - 1) + j);
 #pragma unroll
       for (int j = 0; j < 5; ++j) {
         e0[j] = __ldg(A.qfc + 5 * q + j);
@@ -159,8 +166,10 @@ __device__ __forceinline__ bool sweep_tile_v2(const SweepArgs& A, const int bid,
       const double av = pv[0];
       double al = av, ar = av, six = 0.0;
       if (!flat) {
+        const double* dv = SA + v * T + ci;
         auto win = [&](int j) { return pv[j * SS]; };
-        zone_parabola(win, sc, e0, e1, k, o, al, ar, six);
+        auto dwin = [&](int j) { return dv[j * SS]; };
+        zone_parabola_dm(win, dwin, e0, e1, k, o, al, ar, six);
       }
       L[v] = avg_left(al, ar, six, hs, tw);
       R[v] = avg_right(al, ar, six, hs, tw);
@@ -319,7 +328,7 @@ __device__ __forceinline__ bool sweep_tile_v2(const SweepArgs& A, const int bid,
 
 template <int AXIS, bool DIPOLE, int NP, int TLC, bool EXACT, int MB = 2>
 __global__ void __launch_bounds__(TLC > 0 ? NP * TLC : 512, TLC > 0 ? MB : 1)
-    sweep_kernel_v2(const SweepArgs A) {
+    sweep_kernel_v5(const SweepArgs A) {
   extern __shared__ double smem[];
   __shared__ unsigned long long s_err;
   if (EXACT) {
@@ -327,7 +336,7 @@ __global__ void __launch_bounds__(TLC > 0 ? NP * TLC : 512, TLC > 0 ? MB : 1)
     for (unsigned i = blockIdx.x; i < n; i += gridDim.x) {
       if (threadIdx.x == 0) s_err = kNoError;
       __syncthreads();
-      sweep_tile_v2<AXIS, DIPOLE, NP, TLC, ExactOps>(A, (int)A.redo_list[i], smem, &s_err);
+      sweep_tile_v5<AXIS, DIPOLE, NP, TLC, ExactOps>(A, (int)A.redo_list[i], smem, &s_err);
       __syncthreads();
       if (threadIdx.x == 0 && s_err != kNoError) atomicMin(A.err, s_err);
       __syncthreads();
@@ -336,7 +345,7 @@ __global__ void __launch_bounds__(TLC > 0 ? NP * TLC : 512, TLC > 0 ? MB : 1)
   }
   if (threadIdx.x == 0) s_err = kNoError;
   __syncthreads();
-  const bool bad = sweep_tile_v2<AXIS, DIPOLE, NP, TLC, MainOps>(A, blockIdx.x, smem, &s_err);
+  const bool bad = sweep_tile_v5<AXIS, DIPOLE, NP, TLC, MainOps>(A, blockIdx.x, smem, &s_err);
   if (__syncthreads_or(bad)) {
     if (threadIdx.x == 0) A.redo_list[atomicAdd(A.redo_count, 1u)] = blockIdx.x;
   } else if (threadIdx.x == 0 && s_err != kNoError) {
