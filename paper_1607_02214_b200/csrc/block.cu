@@ -804,10 +804,9 @@ void choose_sweep_tiles(ppmlr_gpu_block* b) {
   // Segments of kSweepTL - 8 = 64 cells (compile-time tile) when the axis is a
   // multiple of 64 or long enough that a partial last segment costs little;
   // otherwise balanced segments of at most Lmax cells (runtime tile).
-  b->sweep_version = env_int("PPMLR_SWEEP_V", 3);
-  // v2 runs one cell per thread: a tile is at most 512 cells (L <= 120)
-  const int Lmax = std::min(env_int("PPMLR_SWEEP_LMAX", 64), b->sweep_version == 1 ? 1 << 20 : 120);
-  const int ipt = b->sweep_version == 1 ? env_int("PPMLR_SWEEP_IPT", 1) : 1;  // v2: 1 cell/thread
+  // one cell per thread: a tile is at most 288 cells (L <= 64)
+  const int Lmax = std::min(env_int("PPMLR_SWEEP_LMAX", 64), kSweepTL - 8);
+  const int ipt = 1;
   const int Lc = kSweepTL - 8;
   for (int a = 0; a < 3; ++a) {
     const int n = b->n[a];
@@ -822,7 +821,7 @@ void choose_sweep_tiles(ppmlr_gpu_block* b) {
     const int T = 4 * (L + 8);
     int nt = (T + ipt - 1) / ipt;
     nt = ((nt + 31) / 32) * 32;
-    b->sweep_threads[a] = std::min(512, std::max(32, nt));
+    b->sweep_threads[a] = std::min(4 * kSweepTL, std::max(32, nt));
   }
 }
 
@@ -866,16 +865,15 @@ int launch_sweep(ppmlr_gpu_block* b, int axis, int phase) {
   A.redo_count = b->d_redo;
   A.redo_list = b->d_redo + 1;
   const int T = 4 * (A.L + 8);
-  const int v = b->sweep_version;
-  const int slots = (v == 2 || v == 4 || v == 5 || v == 6 ? 25 : 33) + (b->with_dipole ? 3 : 0);
+  const int slots = 25 + (b->with_dipole ? 3 : 0);
   const size_t smem = sizeof(double) * (size_t)T * slots;
   // The sweep writes only the interior of the output buffer; its ghost
   // shells stay stale until the next fill (every reader fills first).
   cudaError_t e = b->precision == PPMLR_FAST
                       ? launch_sweep_fast(axis, b->with_dipole, A, b->sweep_threads[axis], smem,
-                                          b->stream, b->sweep_version)
+                                          b->stream)
                       : launch_sweep_strict(axis, b->with_dipole, A, b->sweep_threads[axis],
-                                            smem, b->stream, b->sweep_version);
+                                            smem, b->stream);
   if (e != cudaSuccess) return cuda_fail(e, "sweep kernel launch");
   b->kernel_launches += 2;  // fast pass + exact re-run of flagged tiles
   b->cur ^= 1;

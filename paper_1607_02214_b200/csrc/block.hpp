@@ -92,7 +92,6 @@ struct ppmlr_gpu_block {
   cudaEvent_t ev[8] = {};
   long kernel_launches = 0;              // every kernel this block enqueued
   int sweep_L[3] = {0, 0, 0};            // segment length per axis
-  int sweep_version = 2;                 // tile schedule (sweep.cuh v1 / sweep_v2.cuh)
   int sweep_threads[3] = {0, 0, 0};
 };
 
@@ -102,9 +101,9 @@ int cuda_fail(cudaError_t e, const char* where);
 // Launchers implemented in sweep_*.cu
 struct SweepArgs;
 cudaError_t launch_sweep_strict(int axis, bool dipole, const SweepArgs& a, int threads,
-                                size_t smem, cudaStream_t st, int version);
+                                size_t smem, cudaStream_t st);
 cudaError_t launch_sweep_fast(int axis, bool dipole, const SweepArgs& a, int threads,
-                              size_t smem, cudaStream_t st, int version);
+                              size_t smem, cudaStream_t st);
 }  // namespace ppmlr_b200
 
 namespace ppmlr_b200 {
