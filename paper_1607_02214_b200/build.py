@@ -28,6 +28,8 @@ UNITS = [
     ("block.cu", False, []),
     ("sweep_strict.cu", False, []),
     ("sweep_fast.cu", True, []),
+    ("sources_strict.cu", False, []),
+    ("sources_fast.cu", True, []),
 ]
 HOST_UNITS = ["host.cpp"]
 

@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "block.hpp"
+#include "sources.cuh"
 #include "sweep.cuh"
 
 using namespace ppmlr_b200;
@@ -40,19 +41,6 @@ int cuda_fail(cudaError_t e, const char* where) {
 
 namespace {
 
-constexpr unsigned long long kInfBits = 0x7FF0000000000000ull;
-
-// ------------------------------------------------------------------ layout
-
-struct Lay {
-  int n0, n1, n2;
-  int P0, S1;
-  long long sy, sz, ncell;
-  __host__ __device__ long long idx(int i, int j, int k) const {  // interior coords
-    return (long long)(i + kG) + sy * (j + kG) + sz * (k + kG);
-  }
-};
-
 Lay lay_of(const ppmlr_gpu_block* b) {
   Lay l;
   l.n0 = b->n[0];
@@ -66,9 +54,6 @@ Lay lay_of(const ppmlr_gpu_block* b) {
   return l;
 }
 
-struct Planes {
-  double* f[8];
-};
 Planes planes(double* base, long long ncell) {
   Planes p;
   for (int f = 0; f < 8; ++f) p.f[f] = base + f * ncell;
@@ -76,6 +61,10 @@ Planes planes(double* base, long long ncell) {
 }
 
 // ---------------------------------------------------------------- kernels
+
+
+
+// ------------------------------------------------------------------ layout
 
 // Reference AoS (ghost gr) k-plane chunk -> device SoA (ghost 4).
 __global__ void aos_to_soa_kernel(const double* __restrict__ aos, int nper, Planes dst, Lay L,
@@ -210,69 +199,6 @@ __global__ void wind_fill_kernel(Planes s, Lay L, const double* bd0, const doubl
   }
 }
 
-struct CtxPtrs {
-  unsigned long long* err;
-  unsigned long long* step;
-  unsigned long long* min;
-  double* dt;
-  double* dt_prev;
-  double* time;
-};
-
-// The three CFL candidates of compute_dt (stepper.cpp:128-137) for one cell.
-// Returns false (and the failing axis) on a non-finite candidate.
-template <class Ops>
-__device__ __forceinline__ void cfl_cands(const double* s, double b0, double b1, double b2,
-                                          double d0, double d1, double d2, const KC& c, Ops& o,
-                                          double* cand) {
-  double cf[3];
-  fast_speed3_all(s, b0, b1, b2, c, o, cf);
-  cand[0] = o.dv(d0, fabs(s[1]) + cf[0]);
-  cand[1] = o.dv(d1, fabs(s[2]) + cf[1]);
-  cand[2] = o.dv(d2, fabs(s[3]) + cf[2]);
-}
-
-__device__ __forceinline__ bool cfl_cell(const double* s, double b0, double b1, double b2,
-                                         double d0, double d1, double d2, const KC& c,
-                                         double& mn, int& bad_axis) {
-  double cand[3];
-  FastOps fo;
-  cfl_cands(s, b0, b1, b2, d0, d1, d2, c, fo, cand);
-  if (fo.bad) {
-    ExactOps eo;
-    cfl_cands(s, b0, b1, b2, d0, d1, d2, c, eo, cand);
-  }
-  for (int a = 0; a < 3; ++a)
-    if (!isfinite(cand[a])) {
-      bad_axis = a;
-      return false;
-    }
-  mn = smin(smin(smin(mn, cand[0]), cand[1]), cand[2]);
-  return true;
-}
-
-__device__ __forceinline__ void block_min_commit(double mn, unsigned long long* gmin) {
-  // positive doubles order like their bit patterns
-  unsigned long long bits = __double_as_longlong(mn);
-  for (int o = 16; o > 0; o >>= 1) {
-    const unsigned long long other = __shfl_xor_sync(0xffffffffu, bits, o);
-    bits = other < bits ? other : bits;
-  }
-  __shared__ unsigned long long wmin[32];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  if (lane == 0) wmin[w] = bits;
-  __syncthreads();
-  if (w == 0) {
-    const int nw = (blockDim.x + 31) >> 5;
-    bits = lane < nw ? wmin[lane] : kInfBits;
-    for (int o = 16; o > 0; o >>= 1) {
-      const unsigned long long other = __shfl_xor_sync(0xffffffffu, bits, o);
-      bits = other < bits ? other : bits;
-    }
-    if (lane == 0 && bits != kInfBits) atomicMin(gmin, bits);
-  }
-}
-
 // Standalone compute_dt over the interior; min into ctx.min.
 template <bool DIPOLE>
 __global__ void cfl_kernel(Planes s, Lay L, const double* bd0, const double* bd1,
@@ -310,301 +236,6 @@ __global__ void step_end_kernel(CtxPtrs ctx, double cfl, int close_step, int hav
     *ctx.dt = cfl * __longlong_as_double(*ctx.min);
     *ctx.min = kInfBits;
   }
-}
-
-// stepper.cpp:42-45; den = (hm*hp)*(hm+hp) and its refined reciprocal come
-// from per-position geometry tables.
-template <class Ops>
-__device__ __forceinline__ double central_diff(double fm, double f0, double fp, double hm,
-                                               double hp, double den, double rden, Ops& o) {
-  return o.div(((hm * hm) * fp + ((hp * hp) - (hm * hm)) * f0) - (hp * hp) * fm, den, rden);
-}
-
-__device__ __forceinline__ void cross3(double ax, double ay, double az, double bx, double by,
-                                       double bz, double* o) {
-  o[0] = ay * bz - az * by;
-  o[1] = az * bx - ax * bz;
-  o[2] = ax * by - ay * bx;
-}
-
-// apply_sources (stepper.cpp:141-200) for one cell from its 7-point
-// stencil: own state s[8] and dipole bo[3]; per axis a the minus/plus
-// neighbours' v and B' (nv[a][side][0..5]) and dipole (nbd[a][side][0..2]);
-// the axis geometry hm, hp, den = (hm*hp)*(hm+hp), rden.  Writes the
-// updated primitive state to q; returns cons_to_prim's code.
-template <class Ops>
-__device__ __forceinline__ int source_update(const double* s, const double* bo,
-                                             const double (*nv)[2][6],
-                                             const double (*nbd)[2][3], const double* hm,
-                                             const double* hp, const double* den,
-                                             const double* rden, const KC& c, double dt,
-                                             Ops& o, double* q) {
-  double gb[3][3], ge[3][3];
-  double e0[3];
-  cross3(s[1], s[2], s[3], bo[0], bo[1], bo[2], e0);
-#pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    double em[3], ep[3];
-    cross3(nv[a][0][0], nv[a][0][1], nv[a][0][2], nbd[a][0][0], nbd[a][0][1], nbd[a][0][2], em);
-    cross3(nv[a][1][0], nv[a][1][1], nv[a][1][2], nbd[a][1][0], nbd[a][1][1], nbd[a][1][2], ep);
-#pragma unroll
-    for (int comp = 0; comp < 3; ++comp) {
-      gb[a][comp] = central_diff(nv[a][0][3 + comp], s[4 + comp], nv[a][1][3 + comp], hm[a], hp[a],
-                                 den[a], rden[a], o);
-      ge[a][comp] = central_diff(em[comp], e0[comp], ep[comp], hm[a], hp[a], den[a], rden[a], o);
-    }
-  }
-  const double cb0 = gb[1][2] - gb[2][1], cb1 = gb[2][0] - gb[0][2], cb2 = gb[0][1] - gb[1][0];
-  const double ce0 = ge[1][2] - ge[2][1], ce1 = ge[2][0] - ge[0][2], ce2 = ge[0][1] - ge[1][0];
-  const double div_b = (gb[0][0] + gb[1][1]) + gb[2][2];
-  double sm[3];
-  cross3(cb0, cb1, cb2, bo[0], bo[1], bo[2], sm);
-  sm[0] = o.div(sm[0], c.c.mu0, c.r_mu0);
-  sm[1] = o.div(sm[1], c.c.mu0, c.r_mu0);
-  sm[2] = o.div(sm[2], c.c.mu0, c.r_mu0);
-  const double si0 = ce0 - s[1] * div_b, si1 = ce1 - s[2] * div_b, si2 = ce2 - s[3] * div_b;
-  const double se = ((s[1] * sm[0] + s[2] * sm[1]) + s[3] * sm[2]) +
-                    o.div((s[4] * ce0 + s[5] * ce1) + s[6] * ce2, c.c.mu0, c.r_mu0);
-  double u[8];
-  prim_to_cons3(s, u, c, o);
-  u[1] = u[1] + sm[0] * dt;
-  u[2] = u[2] + sm[1] * dt;
-  u[3] = u[3] + sm[2] * dt;
-  u[4] = u[4] + si0 * dt;
-  u[5] = u[5] + si1 * dt;
-  u[6] = u[6] + si2 * dt;
-  u[7] = u[7] + dt * se;
-  return cons_to_prim3(u, q, c, o);
-}
-
-struct SrcArgs {
-  Planes in, out;
-  Lay L;
-  const double *bd0, *bd1, *bd2;
-  const double *hm0, *hp0, *hm1, *hp1, *hm2, *hp2;  // per axis, ghost-inclusive
-  const double *den0, *den1, *den2, *rden0, *rden1, *rden2;
-  const double *dx0, *dx1, *dx2;
-  // frozen core
-  int fl0, fl1, fl2, fn0, fn1, fn2;
-  const int* fslot;
-  const double* fst;
-  long long nfrozen;
-  Consts c;
-  CtxPtrs ctx;
-  int fuse_cfl;
-  unsigned* redo_count;
-  unsigned* redo_list;
-  unsigned redo_cap;
-};
-
-// apply_sources (stepper.cpp:141-200) + restore_frozen_core (:284-286) +
-// the next step's compute_dt (:119-139), one thread per interior cell.
-// Gathers one cell's 7-point stencil from global memory (EXACT re-run and
-// reference path of the tiled kernel below).
-template <bool DIPOLE>
-__device__ __forceinline__ void gather_stencil(const SrcArgs& A, int i, int j, int k, double* s,
-                                               double* bo, double (*nv)[2][6],
-                                               double (*nbd)[2][3], double* hm, double* hp,
-                                               double* den, double* rden) {
-  const Lay& L = A.L;
-  const long long d = L.idx(i, j, k);
-#pragma unroll
-  for (int f = 0; f < 8; ++f) s[f] = A.in.f[f][d];
-  bo[0] = DIPOLE ? A.bd0[d] : 0.0;
-  bo[1] = DIPOLE ? A.bd1[d] : 0.0;
-  bo[2] = DIPOLE ? A.bd2[d] : 0.0;
-#pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    const long long st = a == 0 ? 1 : (a == 1 ? L.sy : L.sz);
-    const int lc = (a == 0 ? i : (a == 1 ? j : k)) + kG;
-    hm[a] = (a == 0 ? A.hm0 : (a == 1 ? A.hm1 : A.hm2))[lc];
-    hp[a] = (a == 0 ? A.hp0 : (a == 1 ? A.hp1 : A.hp2))[lc];
-    den[a] = (a == 0 ? A.den0 : (a == 1 ? A.den1 : A.den2))[lc];
-    rden[a] = (a == 0 ? A.rden0 : (a == 1 ? A.rden1 : A.rden2))[lc];
-#pragma unroll
-    for (int side = 0; side < 2; ++side) {
-      const long long dn = side == 0 ? d - st : d + st;
-#pragma unroll
-      for (int f = 0; f < 6; ++f) nv[a][side][f] = A.in.f[1 + f][dn];
-      nbd[a][side][0] = DIPOLE ? A.bd0[dn] : 0.0;
-      nbd[a][side][1] = DIPOLE ? A.bd1[dn] : 0.0;
-      nbd[a][side][2] = DIPOLE ? A.bd2[dn] : 0.0;
-    }
-  }
-}
-
-// Epilogue shared by both source kernels: error key, frozen-core override
-// (restore_frozen_core), store, and the next step's CFL candidates.
-template <bool DIPOLE>
-__device__ __forceinline__ void source_epilogue(const SrcArgs& A, const KC& c, int i, int j,
-                                                int k, long long t, const double* s,
-                                                const double* bo, double* q, int bad,
-                                                unsigned long long step, double& mn) {
-  const Lay& L = A.L;
-  if (bad) {
-    atomicMin(A.ctx.err, err_key(step, kPhaseSources, 0,
-                                 ((unsigned long long)t << 2) |
-                                     (bad == 1 ? kErrDensity : kErrPressure)));
-#pragma unroll
-    for (int f = 0; f < 8; ++f) q[f] = s[f];
-  }
-  if (A.nfrozen > 0) {
-    const int fi = i - A.fl0, fj = j - A.fl1, fk = k - A.fl2;
-    if (fi >= 0 && fi < A.fn0 && fj >= 0 && fj < A.fn1 && fk >= 0 && fk < A.fn2) {
-      const int slot = A.fslot[fi + A.fn0 * (fj + A.fn1 * fk)];
-      if (slot >= 0) {
-#pragma unroll
-        for (int f = 0; f < 8; ++f) q[f] = A.fst[f * A.nfrozen + slot];
-      }
-    }
-  }
-  const long long d = L.idx(i, j, k);
-#pragma unroll
-  for (int f = 0; f < 8; ++f) A.out.f[f][d] = q[f];
-  if (A.fuse_cfl) {
-    int badax = 0;
-    if (!cfl_cell(q, bo[0], bo[1], bo[2], A.dx0[i + kG], A.dx1[j + kG], A.dx2[k + kG], c, mn,
-                  badax))
-      atomicMin(A.ctx.err, err_key(step + 1, kPhaseCfl, 0, ((unsigned long long)t * 3 + badax) << 2));
-  }
-}
-
-// EXACT re-run of the cells queued by the tiled kernel (redo list; on
-// overflow every cell), with plain `/` and `sqrt`.
-template <bool DIPOLE>
-__global__ void __launch_bounds__(256, 2) sources_exact_kernel(const SrcArgs A) {
-  const Lay& L = A.L;
-  const KC c = make_kc(A.c);
-  const long long total = (long long)L.n0 * L.n1 * L.n2;
-  double mn = __longlong_as_double(kInfBits);
-  const unsigned long long step = *A.ctx.step;
-  const double dt = *A.ctx.dt;
-  const bool all = *A.redo_count > A.redo_cap;
-  const long long n_items = all ? total : (long long)*A.redo_count;
-  for (long long it = blockIdx.x * (long long)blockDim.x + threadIdx.x; it < n_items;
-       it += (long long)gridDim.x * blockDim.x) {
-    const long long t = all ? it : (long long)A.redo_list[it];
-    const int i = (int)(t % L.n0);
-    const int j = (int)((t / L.n0) % L.n1);
-    const int k = (int)(t / ((long long)L.n0 * L.n1));
-    double s[8], bo[3], nv[3][2][6], nbd[3][2][3], hm[3], hp[3], den[3], rden[3], q[8];
-    gather_stencil<DIPOLE>(A, i, j, k, s, bo, nv, nbd, hm, hp, den, rden);
-    ExactOps eo;
-    const int bad = source_update(s, bo, nv, nbd, hm, hp, den, rden, c, dt, eo, q);
-    source_epilogue<DIPOLE>(A, c, i, j, k, t, s, bo, q, bad, step, mn);
-  }
-  if (A.fuse_cfl) block_min_commit(mn, A.ctx.min);
-}
-
-// apply_sources (stepper.cpp:141-200) + restore_frozen_core (:284-286) +
-// the next step's compute_dt (:119-139), 2.5-D blocked: a CTA owns a 32x8
-// (x, y) tile and marches through a z chunk, keeping the planes z-1, z, z+1
-// (v, B' and the dipole, with a one-cell x/y halo) in a shared-memory ring,
-// so every stencil input is fetched from HBM once.  FastOps; cells whose
-// fast-path guards fail are queued for sources_exact_kernel.
-constexpr int kSrcTX = 32, kSrcTY = 8, kSrcHX = kSrcTX + 2, kSrcHY = kSrcTY + 2;
-
-template <bool DIPOLE>
-__global__ void __launch_bounds__(kSrcTX * kSrcTY, 2) sources_tiled_kernel(const SrcArgs A,
-                                                                            int zchunk) {
-  constexpr int NF = DIPOLE ? 9 : 6;
-  constexpr int PL = kSrcHX * kSrcHY;  // cells per plane (incl. halo)
-  extern __shared__ double ring[];     // [3][NF][PL]
-  const Lay& L = A.L;
-  const KC c = make_kc(A.c);
-  const int tx = threadIdx.x % kSrcTX, ty = threadIdx.x / kSrcTX;
-  const int x0 = blockIdx.x * kSrcTX, y0 = blockIdx.y * kSrcTY;
-  const int z0 = blockIdx.z * zchunk, z1 = min(L.n2, z0 + zchunk);
-  const int i = x0 + tx, j = y0 + ty;
-  const bool in_xy = i < L.n0 && j < L.n1;
-  const unsigned long long step = *A.ctx.step;
-  const double dt = *A.ctx.dt;
-  double mn = __longlong_as_double(kInfBits);
-
-  auto load_plane = [&](int z, int slot) {
-    double* dstp = ring + (size_t)slot * NF * PL;
-    for (int c2 = threadIdx.x; c2 < PL; c2 += blockDim.x) {
-      const int xx = c2 % kSrcHX, yy = c2 / kSrcHX;
-      const bool corner = (xx == 0 || xx == kSrcHX - 1) && (yy == 0 || yy == kSrcHY - 1);
-      if (corner) continue;
-      const long long d = L.idx(x0 - 1 + xx, y0 - 1 + yy, z);
-#pragma unroll
-      for (int f = 0; f < 6; ++f) dstp[f * PL + c2] = A.in.f[1 + f][d];
-      if (DIPOLE) {
-        dstp[6 * PL + c2] = A.bd0[d];
-        dstp[7 * PL + c2] = A.bd1[d];
-        dstp[8 * PL + c2] = A.bd2[d];
-      }
-    }
-  };
-  load_plane(z0 - 1, (z0 + 2) % 3);
-  load_plane(z0, z0 % 3);
-  // per-thread constant geometry along x and y
-  double hm[3], hp[3], den[3], rden[3];
-  if (in_xy) {
-    hm[0] = A.hm0[i + kG];
-    hp[0] = A.hp0[i + kG];
-    den[0] = A.den0[i + kG];
-    rden[0] = A.rden0[i + kG];
-    hm[1] = A.hm1[j + kG];
-    hp[1] = A.hp1[j + kG];
-    den[1] = A.den1[j + kG];
-    rden[1] = A.rden1[j + kG];
-  }
-  const int cc = (ty + 1) * kSrcHX + (tx + 1);  // this cell in a plane
-  for (int k = z0; k < z1; ++k) {
-    load_plane(k + 1, (k + 1) % 3);
-    __syncthreads();
-    if (in_xy) {
-      const double* pm = ring + (size_t)((k + 2) % 3) * NF * PL;
-      const double* p0 = ring + (size_t)(k % 3) * NF * PL;
-      const double* pp = ring + (size_t)((k + 1) % 3) * NF * PL;
-      const long long d = L.idx(i, j, k);
-      double s[8], bo[3], nv[3][2][6], nbd[3][2][3], q[8];
-      s[0] = A.in.f[0][d];
-      s[7] = A.in.f[7][d];
-#pragma unroll
-      for (int f = 0; f < 6; ++f) s[1 + f] = p0[f * PL + cc];
-#pragma unroll
-      for (int f = 0; f < 3; ++f) bo[f] = DIPOLE ? p0[(6 + f) * PL + cc] : 0.0;
-      const int nb_off[2][2] = {{cc - 1, cc + 1}, {cc - kSrcHX, cc + kSrcHX}};
-#pragma unroll
-      for (int a = 0; a < 2; ++a)
-#pragma unroll
-        for (int side = 0; side < 2; ++side) {
-#pragma unroll
-          for (int f = 0; f < 6; ++f) nv[a][side][f] = p0[f * PL + nb_off[a][side]];
-#pragma unroll
-          for (int f = 0; f < 3; ++f)
-            nbd[a][side][f] = DIPOLE ? p0[(6 + f) * PL + nb_off[a][side]] : 0.0;
-        }
-#pragma unroll
-      for (int f = 0; f < 6; ++f) {
-        nv[2][0][f] = pm[f * PL + cc];
-        nv[2][1][f] = pp[f * PL + cc];
-      }
-#pragma unroll
-      for (int f = 0; f < 3; ++f) {
-        nbd[2][0][f] = DIPOLE ? pm[(6 + f) * PL + cc] : 0.0;
-        nbd[2][1][f] = DIPOLE ? pp[(6 + f) * PL + cc] : 0.0;
-      }
-      hm[2] = A.hm2[k + kG];
-      hp[2] = A.hp2[k + kG];
-      den[2] = A.den2[k + kG];
-      rden[2] = A.rden2[k + kG];
-      FastOps fo;
-      const int bad = source_update(s, bo, nv, nbd, hm, hp, den, rden, c, dt, fo, q);
-      const long long t = (long long)i + (long long)L.n0 * ((long long)j + (long long)L.n1 * k);
-      if (fo.bad) {
-        const unsigned slot = atomicAdd(A.redo_count, 1u);
-        if (slot < A.redo_cap) A.redo_list[slot] = (unsigned)t;
-      } else {
-        source_epilogue<DIPOLE>(A, c, i, j, k, t, s, bo, q, bad, step, mn);
-      }
-    }
-    __syncthreads();
-  }
-  if (A.fuse_cfl) block_min_commit(mn, A.ctx.min);
 }
 
 // In-place refined reciprocals of a geometry table.
@@ -954,23 +585,10 @@ int launch_sources(ppmlr_gpu_block* b, int fuse_cfl) {
   A.redo_list = b->d_redo + 1;
   A.redo_cap = b->redo_cap;
   CK(cudaMemsetAsync(b->d_redo, 0, sizeof(unsigned), b->stream));
-  const int zchunk = std::min(b->n[2], 32);
-  const dim3 grid((b->n[0] + kSrcTX - 1) / kSrcTX, (b->n[1] + kSrcTY - 1) / kSrcTY,
-                  (b->n[2] + zchunk - 1) / zchunk);
-  const int nf = b->with_dipole ? 9 : 6;
-  const size_t smem = sizeof(double) * 3 * nf * kSrcHX * kSrcHY;
-  if (b->with_dipole) {
-    CK(cudaFuncSetAttribute(sources_tiled_kernel<true>,
-                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    sources_tiled_kernel<true><<<grid, kSrcTX * kSrcTY, smem, b->stream>>>(A, zchunk);
-    sources_exact_kernel<true><<<148, 256, 0, b->stream>>>(A);
-  } else {
-    CK(cudaFuncSetAttribute(sources_tiled_kernel<false>,
-                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    sources_tiled_kernel<false><<<grid, kSrcTX * kSrcTY, smem, b->stream>>>(A, zchunk);
-    sources_exact_kernel<false><<<148, 256, 0, b->stream>>>(A);
-  }
-  CK(cudaGetLastError());
+  const cudaError_t e = b->precision == PPMLR_FAST
+                            ? launch_sources_fast(A, b->with_dipole, b->stream)
+                            : launch_sources_strict(A, b->with_dipole, b->stream);
+  if (e != cudaSuccess) return cuda_fail(e, "sources kernel launch");
   b->kernel_launches += 2;
   b->cur ^= 1;
   return 0;

@@ -11,7 +11,6 @@
 
 namespace ppmlr_b200 {
 
-constexpr int kG = 4;  // device ghost width (the dependency window)
 
 // Per-axis device geometry, ghost-inclusive with kG ghosts (span = n + 8).
 struct DevAxis {
@@ -102,6 +101,9 @@ int cuda_fail(cudaError_t e, const char* where);
 struct SweepArgs;
 cudaError_t launch_sweep_strict(int axis, bool dipole, const SweepArgs& a, int threads,
                                 size_t smem, cudaStream_t st);
+struct SrcArgs;
+cudaError_t launch_sources_strict(const SrcArgs& a, bool dipole, cudaStream_t st);
+cudaError_t launch_sources_fast(const SrcArgs& a, bool dipole, cudaStream_t st);
 cudaError_t launch_sweep_fast(int axis, bool dipole, const SweepArgs& a, int threads,
                               size_t smem, cudaStream_t st);
 }  // namespace ppmlr_b200

@@ -11,6 +11,8 @@
 
 namespace ppmlr_b200 {
 
+constexpr int kG = 4;  // device ghost width (the dependency window)
+
 struct Consts {
   double gamma, mu0, pressure_floor;
   double gm1;      // gamma - 1.0   (hoisted; same rounding as the reference's inline form)
