@@ -379,3 +379,38 @@ def test_pack_unpack_slabs_in_reference_order(gpu):
             sl2 = list(sl)
             sl2[2 - a] = slice(lo2, lo2 + layers)
             assert bits_equal(after[tuple(sl2)], full[tuple(sl)]), (face, layers)
+
+
+def test_distributed_driver_single_rank_nccl(gpu):
+    """dist.py on the device with a world-size-1 NCCL group: the block's dt
+    slot is all-reduced in place through torch (via __cuda_array_interface__),
+    kernels run on torch's stream, and the result equals the in-process
+    harness bit for bit.  (Multi-rank exchanges are covered by the gloo test
+    tests/test_dist_cpu.py; this pool exposes one GPU.)"""
+    import os
+    import socket
+    import torch
+    import torch.distributed as dist
+    from paper_1607_02214_b200 import configs
+    from paper_1607_02214_b200 import dist as pdist
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        cfg = configs.magnetosphere_small()
+        blk = pdist.DeviceRankBlock(cfg.specs, (1, 1, 1), cfg.options, 0, cfg.ic, 0)
+        ex = pdist.Exchanger(blk.info, blk.n, lambda n: torch.empty(n, dtype=torch.float64,
+                                                                    device="cuda"))
+        pdist.run_rank(blk, ex, 5, 0, cfg.options.cfl, cfg.options.with_sources)
+        torch.cuda.synchronize()
+        blk.check()
+        got = blk.interior()
+        blk.close()
+    finally:
+        dist.destroy_process_group()
+    h = _harness(gpu, cfg.specs, cfg.options, cfg.ic)
+    h.run(5)
+    assert bits_equal(got, h.gather_interior())
