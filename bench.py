@@ -243,11 +243,13 @@ def bench_single(args):
     frac_hbm = (sweep_bytes / avg_sweep_s) / (hbm * 1e9)
     frac_fp64 = (sweep_flops / avg_sweep_s) / (peak_fp64 * 1e12)
     bound = "fp64" if frac_fp64 >= frac_hbm else "hbm"
-    traffic = None
+    traffic = None  # dram__bytes_read+write per sweep launch, from an ncu --set full capture
     prof = os.path.join(ROOT, "profiles", "ncu_sweep_traffic.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get(args.config, {}).get(args.precision)
+            rec = json.load(open(prof)).get(kind, {})
+            if "bytes_per_cell" in rec:
+                traffic = rec["bytes_per_cell"] * cells
         except Exception:
             traffic = None
     roofline = {
@@ -368,6 +370,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="blast512")
     ap.add_argument("--precision", default="fast", choices=["strict", "fast"])
+    ap.add_argument("--force-dist", action="store_true",
+                    help="run the torch.distributed (NCCL) driver even on one rank")
     ap.add_argument("--no-secondary", action="store_true",
                     help="skip the timing of the other precision mode")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -379,7 +383,7 @@ def main():
     if args.impl == "reference":
         return bench_reference(args)
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    if world > 1 or args.gpus > 1:
+    if world > 1 or args.gpus > 1 or args.force_dist:
         from paper_1607_02214_b200 import dist
         return dist.bench_distributed(args, METRIC, UNIT, ALG, make_config, ClockSampler,
                                       fp64_peak_tflops, measured_peaks, cpu_baseline)
