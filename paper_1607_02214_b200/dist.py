@@ -212,9 +212,12 @@ def bench_distributed(args, METRIC, UNIT, ALG, make_config, ClockSampler, fp64_p
     """bench.py's N-GPU arm: weak scaling, one 512^3 x-slab per rank."""
     import torch
     import torch.distributed as dist
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    for k, v in (("RANK", "0"), ("WORLD_SIZE", "1"), ("LOCAL_RANK", "0"),
+                 ("MASTER_ADDR", "127.0.0.1"), ("MASTER_PORT", "29511")):
+        os.environ.setdefault(k, v)  # allow a single-rank run outside torchrun
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
+    local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg, kind = make_config(args.config, world)
