@@ -806,38 +806,18 @@ static int ensure_scratch(ppmlr_gpu_block* b, size_t bytes) {
   return 0;
 }
 
-int ppmlr_gpu_block_upload(ppmlr_gpu_block* b, const double* fields, const double* bd,
-                           const int64_t* frozen_idx, const double* frozen_states,
-                           int64_t n_frozen) {
-  CK(cudaSetDevice(b->device));
-  CK(cudaStreamSynchronize(b->stream));
+}  // extern "C"
+
+namespace ppmlr_b200 {
+
+// Frozen inner core (init_magnetosphere, stepper.cpp:107-110): bounding-box
+// slot map + SoA states on the device; linear indices in the caller's
+// (ghost g_ref) layout.
+int block_set_frozen(ppmlr_gpu_block* b, const int64_t* frozen_idx, const double* frozen_states,
+                     int64_t n_frozen) {
   const int gr = b->g_ref;
-  const int S0r = b->n[0] + 2 * gr, S1r = b->n[1] + 2 * gr, S2r = b->n[2] + 2 * gr;
-  const size_t plane = (size_t)S0r * S1r;
-  const int kchunk = (int)std::max<size_t>(1, std::min<size_t>(S2r, (64ull << 20) / (plane * 64)));
-  if (int rc = ensure_scratch(b, plane * kchunk * 8 * sizeof(double))) return rc;
+  const int S0r = b->n[0] + 2 * gr, S1r = b->n[1] + 2 * gr;
   const Lay L = lay_of(b);
-  for (int which = 0; which < 2; ++which) {
-    const double* src = which == 0 ? fields : bd;
-    if (!src) continue;
-    if (which == 1 && !b->with_dipole) continue;
-    const int nper = which == 0 ? 8 : 3;
-    for (int kr0 = 0; kr0 < S2r; kr0 += kchunk) {
-      const int nk = std::min(kchunk, S2r - kr0);
-      CK(cudaMemcpyAsync(b->d_scratch, src + plane * kr0 * nper, plane * nk * nper * 8,
-                         cudaMemcpyHostToDevice, b->stream));
-      for (int k = 0; k < 2; ++k) {
-        if (which == 1 && k == 1) break;
-        aos_to_soa_kernel<<<grid_for(plane * nk), 256, 0, b->stream>>>(
-            which == 0 ? b->d_scratch : nullptr, nper, planes(b->buf[k], b->ncell), L, gr, S0r,
-            S1r, kr0, nk, which == 1 ? b->d_scratch : nullptr, b->bd, b->bd + b->ncell,
-            b->bd + 2 * b->ncell);
-      }
-      CK(cudaGetLastError());
-      CK(cudaStreamSynchronize(b->stream));
-    }
-  }
-  // frozen core: bounding box slot map + SoA states
   cudaFree(b->fslot);
   cudaFree(b->fstates);
   cudaFree(b->fidx);
@@ -885,6 +865,63 @@ int ppmlr_gpu_block_upload(ppmlr_gpu_block* b, const double* fields, const doubl
     if (int rc = upload_vec(&b->fstates, st)) return rc;
     if (int rc = upload_vec(&b->fidx, didx)) return rc;
   }
+  return 0;
+}
+
+// Streamed upload: `fill(kr0, nk, fields, bd)` writes reference-layout AoS
+// k-planes [kr0, kr0+nk) (bd only when the block carries the dipole) into
+// pinned staging; each chunk is copied and converted while the next is
+// filled.  No full-size host copy of the state is needed.
+int block_upload_streamed(ppmlr_gpu_block* b, const ChunkFill& fill, bool with_bd) {
+  CK(cudaSetDevice(b->device));
+  CK(cudaStreamSynchronize(b->stream));
+  const int gr = b->g_ref;
+  const int S0r = b->n[0] + 2 * gr, S1r = b->n[1] + 2 * gr, S2r = b->n[2] + 2 * gr;
+  const size_t plane = (size_t)S0r * S1r;
+  with_bd = with_bd && b->with_dipole && b->bd;
+  const int nper = with_bd ? 11 : 8;
+  const int kchunk = (int)std::max<size_t>(1, std::min<size_t>(S2r, (64ull << 20) / (plane * 8 * nper)));
+  const size_t chunk_doubles = plane * kchunk * nper;
+  if (int rc = ensure_scratch(b, 2 * chunk_doubles * sizeof(double))) return rc;
+  double* host[2] = {nullptr, nullptr};
+  cudaEvent_t done[2] = {nullptr, nullptr};
+  for (int q = 0; q < 2; ++q) {
+    CK(cudaMallocHost(&host[q], chunk_doubles * sizeof(double)));
+    CK(cudaEventCreateWithFlags(&done[q], cudaEventDisableTiming));
+  }
+  const Lay L = lay_of(b);
+  int rc = 0;
+  int q = 0;
+  for (int kr0 = 0; kr0 < S2r && !rc; kr0 += kchunk, q ^= 1) {
+    const int nk = std::min(kchunk, S2r - kr0);
+    CK(cudaEventSynchronize(done[q]));  // staging buffer q free again
+    double* hf = host[q];
+    double* hb = with_bd ? host[q] + plane * nk * 8 : nullptr;
+    fill(kr0, nk, hf, hb);
+    double* dscr = b->d_scratch + q * chunk_doubles;
+    CK(cudaMemcpyAsync(dscr, hf, plane * nk * nper * sizeof(double), cudaMemcpyHostToDevice,
+                       b->stream));
+    for (int k = 0; k < 2; ++k)
+      aos_to_soa_kernel<<<grid_for(plane * nk), 256, 0, b->stream>>>(
+          dscr, 8, planes(b->buf[k], b->ncell), L, gr, S0r, S1r, kr0, nk,
+          (k == 0 && hb) ? dscr + plane * nk * 8 : nullptr, b->bd,
+          b->bd ? b->bd + b->ncell : nullptr, b->bd ? b->bd + 2 * b->ncell : nullptr);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaEventRecord(done[q], b->stream);
+    if (e != cudaSuccess) rc = cuda_fail(e, "streamed upload");
+  }
+  cudaStreamSynchronize(b->stream);
+  for (int k = 0; k < 2; ++k) {
+    cudaFreeHost(host[k]);
+    cudaEventDestroy(done[k]);
+  }
+  if (rc) return rc;
+  return block_finish_upload(b);
+}
+
+// Pre-filled sunward shell, fresh error window and step counter.
+int block_finish_upload(ppmlr_gpu_block* b) {
+  const Lay L = lay_of(b);
   // Magnetosphere: constant sunward shell in both buffers.
   if (b->boundary == PPMLR_BC_MAGNETOSPHERE && b->physical[0][1]) {
     for (int k = 0; k < 2; ++k)
@@ -902,6 +939,23 @@ int ppmlr_gpu_block_upload(ppmlr_gpu_block* b, const double* fields, const doubl
   b->step_base = 0;
   CK(cudaStreamSynchronize(b->stream));
   return 0;
+}
+
+}  // namespace ppmlr_b200
+
+extern "C" {
+
+int ppmlr_gpu_block_upload(ppmlr_gpu_block* b, const double* fields, const double* bd,
+                           const int64_t* frozen_idx, const double* frozen_states,
+                           int64_t n_frozen) {
+  const int gr = b->g_ref;
+  const size_t plane = (size_t)(b->n[0] + 2 * gr) * (b->n[1] + 2 * gr);
+  const bool with_bd = b->with_dipole && bd != nullptr;
+  if (int rc = block_set_frozen(b, frozen_idx, frozen_states, n_frozen)) return rc;
+  return block_upload_streamed(b, [&](int kr0, int nk, double* hf, double* hb) {
+    std::memcpy(hf, fields + plane * kr0 * 8, plane * nk * 8 * sizeof(double));
+    if (hb) std::memcpy(hb, bd + plane * kr0 * 3, plane * nk * 3 * sizeof(double));
+  }, with_bd);
 }
 
 static int download_impl(ppmlr_gpu_block* b, double* fields, bool interior_only) {

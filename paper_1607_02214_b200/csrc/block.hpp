@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -117,4 +118,13 @@ int launch_frozen(ppmlr_gpu_block* b);
 int launch_cfl(ppmlr_gpu_block* b, unsigned long long step_add);
 int launch_step_end(ppmlr_gpu_block* b, double cfl, int close_step, int have_min);
 int block_set_dt(ppmlr_gpu_block* b, double dt);  // dt < 0: keep the device slot
+
+// Streamed state upload (block.cu).  `fill(kr0, nk, fields, bd)` writes the
+// reference-layout (ghost g_ref) AoS k-planes [kr0, kr0 + nk): 8 doubles per
+// cell into `fields`, 3 per cell into `bd` when `bd` is non-null.
+using ChunkFill = std::function<void(int kr0, int nk, double* fields, double* bd)>;
+int block_set_frozen(ppmlr_gpu_block* b, const int64_t* frozen_idx, const double* frozen_states,
+                     int64_t n_frozen);
+int block_upload_streamed(ppmlr_gpu_block* b, const ChunkFill& fill, bool with_bd);
+int block_finish_upload(ppmlr_gpu_block* b);
 }  // namespace ppmlr_b200

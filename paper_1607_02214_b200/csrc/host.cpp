@@ -16,6 +16,7 @@
 #include <cstring>
 #include <functional>
 #include <stdexcept>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -369,6 +370,12 @@ std::function<Prim(const V3&)> make_ic(int kind, const double* p) {
   }
 }
 
+std::function<Prim(const V3&)> ic_of(int kind, const double* params) {
+  double p[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (params) std::memcpy(p, params, sizeof p);
+  return make_ic(kind, p);
+}
+
 struct HostBlock {
   int n[3], lo[3], g;
   std::vector<double> cen[3], spc[3];
@@ -378,79 +385,146 @@ struct HostBlock {
   }
 };
 
-// make_block's dipole (stepper.cpp:63-69), ghosts included.
+// make_block's dipole (stepper.cpp:63-69) at one ghost-inclusive cell.
+inline void dipole_cell(const HostBlock& hb, double mu0, int i, int j, int k, double* o) {
+  const V3 v = dipole(hb.center(i, j, k), kMoment, mu0);
+  o[0] = v.x;
+  o[1] = v.y;
+  o[2] = v.z;
+}
+
+struct MagnetosphereProfile {
+  double rho_core, p_core, falloff, r_ref;
+};
+
+// init_magnetosphere (stepper.cpp:83-112) at one ghost-inclusive cell;
+// `bd` is that cell's dipole (null without it).  Returns whether the cell
+// belongs to the frozen inner core (interior and r < 3).
+inline bool magnetosphere_cell(const HostBlock& hb, const ppmlr_gpu_options& o,
+                               const MagnetosphereProfile& mp, const double* bd, int i, int j,
+                               int k, double* s) {
+  const int g = hb.g;
+  const int S0 = hb.n[0] + 2 * g, S1 = hb.n[1] + 2 * g, S2 = hb.n[2] + 2 * g;
+  const V3 image_m{-kMoment.x, kMoment.y, kMoment.z};
+  const V3 pos = hb.center(i, j, k);
+  for (int q = 0; q < 8; ++q) s[q] = 0.0;
+  if (pos.x <= 15.0) {
+    const double nrm = std::sqrt(dot3(pos, pos));
+    const double rr = std::max(nrm, 1e-6);
+    const double shape = std::pow(mp.r_ref / std::max(rr, mp.r_ref), mp.falloff);
+    s[0] = mp.rho_core * shape;
+    s[7] = mp.p_core * shape;
+    const V3 b = dipole({pos.x - 30.0, pos.y - 0.0, pos.z - 0.0}, image_m, o.mu0);
+    s[4] = b.x;
+    s[5] = b.y;
+    s[6] = b.z;
+  } else {
+    s[0] = o.wind_rho;
+    s[7] = o.wind_p;
+    for (int a = 0; a < 3; ++a) {
+      s[1 + a] = o.wind_v[a];
+      s[4 + a] = o.wind_imf[a] - (bd ? bd[a] : 0.0);
+    }
+  }
+  const bool interior = i >= g && i < S0 - g && j >= g && j < S1 - g && k >= g && k < S2 - g;
+  return interior && std::sqrt(dot3(pos, pos)) < 3.0;
+}
+
+// Runs fn(k, j, row_index) over the ghost-inclusive rows of k-planes
+// [k0, k0 + nk) on worker threads; each worker owns a contiguous run of
+// rows, so per-worker outputs concatenate back in (k, j, i) order.
+void for_rows(const HostBlock& hb, int k0, int nk,
+              const std::function<void(int w, int k, int j)>& fn, int nworkers) {
+  const int S1 = hb.n[1] + 2 * hb.g;
+  const long rows = (long)nk * S1;
+  auto work = [&](int w) {
+    const long r0 = rows * w / nworkers, r1 = rows * (w + 1) / nworkers;
+    for (long r = r0; r < r1; ++r) fn(w, k0 + (int)(r / S1), (int)(r % S1));
+  };
+  if (nworkers == 1) {
+    work(0);
+    return;
+  }
+  std::vector<std::thread> pool;
+  for (int w = 1; w < nworkers; ++w) pool.emplace_back(work, w);
+  work(0);
+  for (auto& t : pool) t.join();
+}
+
+int init_workers() {
+  const unsigned hw = std::thread::hardware_concurrency();
+  return (int)std::max(1u, std::min(hw == 0 ? 1u : hw, 32u));
+}
+
+// Fills one k-chunk of the reference AoS layout (8 doubles per cell, plus
+// the dipole when `bd` is non-null).  kind < 0: init_magnetosphere (frozen
+// cells appended in (k, j, i) order); kind == -2: make_block's default
+// {1, 0, 0, 1}; kind >= 0: init_with(make_ic(kind)).
+struct ChunkInit {
+  const HostBlock* hb;
+  const ppmlr_gpu_options* o;
+  int kind;
+  MagnetosphereProfile mp{};
+  std::function<Prim(const V3&)> ic;
+  std::vector<int64_t>* fidx = nullptr;
+  std::vector<double>* fst = nullptr;
+
+  void operator()(int kr0, int nk, double* f, double* bd) const {
+    const HostBlock& b = *hb;
+    const int S0 = b.n[0] + 2 * b.g, S1 = b.n[1] + 2 * b.g;
+    const int nw = (int)std::max(1L, std::min<long>(init_workers(), (long)nk * S1 / 4));
+    std::vector<std::vector<int64_t>> wi(nw);
+    std::vector<std::vector<double>> ws(nw);
+    const bool need_bd = o->with_dipole && (bd || kind == -1);
+    for_rows(b, kr0, nk, [&](int w, int k, int j) {
+      double dloc[3];
+      for (int i = 0; i < S0; ++i) {
+        const size_t loc = (size_t)i + (size_t)S0 * (j + (size_t)S1 * (k - kr0));
+        double* bc = nullptr;
+        if (need_bd) {
+          bc = bd ? bd + 3 * loc : dloc;
+          dipole_cell(b, o->mu0, i, j, k, bc);
+        }
+        double* s = f + 8 * loc;
+        if (kind == -1) {
+          if (magnetosphere_cell(b, *o, mp, bc, i, j, k, s)) {
+            wi[w].push_back((int64_t)i + (int64_t)S0 * (j + (int64_t)S1 * k));
+            ws[w].insert(ws[w].end(), s, s + 8);
+          }
+        } else if (kind == -2) {
+          for (int q = 0; q < 8; ++q) s[q] = 0.0;
+          s[0] = 1.0;
+          s[7] = 1.0;
+        } else {
+          const Prim p = ic(b.center(i, j, k));
+          std::memcpy(s, p.s, 64);
+        }
+      }
+    }, nw);
+    if (fidx)
+      for (int w = 0; w < nw; ++w) {
+        fidx->insert(fidx->end(), wi[w].begin(), wi[w].end());
+        fst->insert(fst->end(), ws[w].begin(), ws[w].end());
+      }
+  }
+};
+
+// Whole-block versions (ppmlr_host_block_state, block geometry queries).
 void block_dipole(const HostBlock& hb, double mu0, std::vector<double>& bd) {
   const int S0 = hb.n[0] + 2 * hb.g, S1 = hb.n[1] + 2 * hb.g, S2 = hb.n[2] + 2 * hb.g;
   bd.assign((size_t)S0 * S1 * S2 * 3, 0.0);
   for (int k = 0; k < S2; ++k)
     for (int j = 0; j < S1; ++j)
-      for (int i = 0; i < S0; ++i) {
-        const V3 v = dipole(hb.center(i, j, k), kMoment, mu0);
-        double* o = &bd[3 * ((size_t)i + (size_t)S0 * (j + (size_t)S1 * k))];
-        o[0] = v.x;
-        o[1] = v.y;
-        o[2] = v.z;
-      }
+      for (int i = 0; i < S0; ++i)
+        dipole_cell(hb, mu0, i, j, k, &bd[3 * ((size_t)i + (size_t)S0 * (j + (size_t)S1 * k))]);
 }
 
-// init_magnetosphere (stepper.cpp:83-112).
-void block_magnetosphere(const HostBlock& hb, const ppmlr_gpu_options& o,
-                         const std::vector<double>& bd, double rho_core, double p_core,
-                         double falloff, double r_ref, std::vector<double>& f,
-                         std::vector<int64_t>& fidx, std::vector<double>& fst) {
-  const int g = hb.g;
-  const int S0 = hb.n[0] + 2 * g, S1 = hb.n[1] + 2 * g, S2 = hb.n[2] + 2 * g;
-  const V3 image_m{-kMoment.x, kMoment.y, kMoment.z};
+void block_fill(const HostBlock& hb, const ChunkInit& ci, std::vector<double>& f,
+                std::vector<double>* bd) {
+  const int S2 = hb.n[2] + 2 * hb.g;
   f.assign(hb.cells() * 8, 0.0);
-  fidx.clear();
-  fst.clear();
-  for (int k = 0; k < S2; ++k)
-    for (int j = 0; j < S1; ++j)
-      for (int i = 0; i < S0; ++i) {
-        const V3 pos = hb.center(i, j, k);
-        const size_t idx = (size_t)i + (size_t)S0 * (j + (size_t)S1 * k);
-        double* s = &f[8 * idx];
-        if (pos.x <= 15.0) {
-          const double nrm = std::sqrt(dot3(pos, pos));
-          const double rr = std::max(nrm, 1e-6);
-          const double shape = std::pow(r_ref / std::max(rr, r_ref), falloff);
-          s[0] = rho_core * shape;
-          s[7] = p_core * shape;
-          const V3 b = dipole({pos.x - 30.0, pos.y - 0.0, pos.z - 0.0}, image_m, o.mu0);
-          s[4] = b.x;
-          s[5] = b.y;
-          s[6] = b.z;
-        } else {
-          s[0] = o.wind_rho;
-          s[7] = o.wind_p;
-          for (int a = 0; a < 3; ++a) {
-            s[1 + a] = o.wind_v[a];
-            s[4 + a] = o.wind_imf[a] - (bd.empty() ? 0.0 : bd[3 * idx + a]);
-          }
-        }
-        const bool interior =
-            i >= g && i < S0 - g && j >= g && j < S1 - g && k >= g && k < S2 - g;
-        if (interior && std::sqrt(dot3(pos, pos)) < 3.0) {
-          fidx.push_back((int64_t)idx);
-          fst.insert(fst.end(), s, s + 8);
-        }
-      }
-}
-
-// init_with (harness.cpp:35-43): the IC at every cell including ghosts.
-void block_ic(const HostBlock& hb, int kind, const double* params, std::vector<double>& f) {
-  double p[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  if (params) std::memcpy(p, params, sizeof p);
-  const auto ic = make_ic(kind, p);
-  const int g = hb.g;
-  const int S0 = hb.n[0] + 2 * g, S1 = hb.n[1] + 2 * g, S2 = hb.n[2] + 2 * g;
-  f.assign(hb.cells() * 8, 0.0);
-  for (int k = 0; k < S2; ++k)
-    for (int j = 0; j < S1; ++j)
-      for (int i = 0; i < S0; ++i) {
-        const Prim q = ic(hb.center(i, j, k));
-        std::memcpy(&f[8 * ((size_t)i + (size_t)S0 * (j + (size_t)S1 * k))], q.s, 64);
-      }
+  if (bd) bd->assign(hb.cells() * 3, 0.0);
+  ci(0, S2, f.data(), bd ? bd->data() : nullptr);
 }
 
 HostBlock host_block(const Axis* ax, const BlockPlan& p, int g) {
@@ -476,7 +550,6 @@ struct ppmlr_gpu_harness {
   ppmlr_gpu_options o{};
   std::vector<ppmlr_gpu_block*> blocks;
   std::vector<std::vector<double>> cen[3], spc[3];  // per block, ghost-inclusive (g_ref)
-  std::vector<std::vector<double>> bd;              // per block AoS (with_dipole)
   std::vector<std::vector<int64_t>> fidx;
   std::vector<std::vector<double>> fst;
   long step = 0;
@@ -497,12 +570,24 @@ struct ppmlr_gpu_harness {
 
 namespace {
 
-int upload_block(ppmlr_gpu_harness* h, int r, const std::vector<double>& f) {
+// Streams block r's initial state to the device chunk by chunk (the host
+// never holds the whole block); the frozen core is collected on the way.
+void upload_init(ppmlr_gpu_harness* h, int r, ChunkInit ci, bool with_bd) {
+  const HostBlock hb = host_block(h->ax, h->plan[r], h->g());
+  ci.hb = &hb;
+  ci.o = &h->o;
+  h->fidx[r].clear();
+  h->fst[r].clear();
+  if (ci.kind == -1) {
+    ci.fidx = &h->fidx[r];
+    ci.fst = &h->fst[r];
+  }
+  ppmlr_gpu_block* b = h->blocks[r];
+  if (int e = block_upload_streamed(b, ci, with_bd)) throw SpecError(e, ppmlr_gpu_last_error());
   const auto& fi = h->fidx[r];
-  return ppmlr_gpu_block_upload(h->blocks[r], f.data(),
-                                h->o.with_dipole ? h->bd[r].data() : nullptr,
-                                fi.empty() ? nullptr : fi.data(),
-                                fi.empty() ? nullptr : h->fst[r].data(), (int64_t)fi.size());
+  if (int e = block_set_frozen(b, fi.empty() ? nullptr : fi.data(),
+                               fi.empty() ? nullptr : h->fst[r].data(), (int64_t)fi.size()))
+    throw SpecError(e, ppmlr_gpu_last_error());
 }
 
 // Ledger entry of one exchange_step (exchange.cpp:93-149): every interior
@@ -595,12 +680,20 @@ int ppmlr_host_block_state(const ppmlr_axis_spec specs[3], int px, int py, int p
     const HostBlock hb = host_block(ax, plan[rank], opts->ghost);
     std::vector<double> bdv, f, fst;
     std::vector<int64_t> fidx;
-    if (opts->with_dipole) block_dipole(hb, opts->mu0, bdv);
-    if (ic_kind < 0)
-      block_magnetosphere(hb, *opts, bdv, params ? params[0] : 1.0, params ? params[1] : 0.1,
-                          params ? params[2] : 3.0, params ? params[3] : 3.0, f, fidx, fst);
-    else
-      block_ic(hb, ic_kind, params, f);
+    ChunkInit ci;
+    ci.hb = &hb;
+    ci.o = opts;
+    if (ic_kind < 0) {
+      ci.kind = -1;
+      ci.mp = {params ? params[0] : 1.0, params ? params[1] : 0.1, params ? params[2] : 3.0,
+               params ? params[3] : 3.0};
+      ci.fidx = &fidx;
+      ci.fst = &fst;
+    } else {
+      ci.kind = ic_kind;
+      ci.ic = ic_of(ic_kind, params);
+    }
+    block_fill(hb, ci, f, opts->with_dipole ? &bdv : nullptr);
     if (fields) std::copy(f.begin(), f.end(), fields);
     if (bd && !bdv.empty()) std::copy(bdv.begin(), bdv.end(), bd);
     if (frozen_idx) std::copy(fidx.begin(), fidx.end(), frozen_idx);
@@ -666,7 +759,6 @@ int ppmlr_gpu_harness_create(const ppmlr_axis_spec specs[3], int px, int py, int
       h->cen[a].resize(nb);
       h->spc[a].resize(nb);
     }
-    h->bd.resize(nb);
     h->fidx.resize(nb);
     h->fst.resize(nb);
     for (size_t r = 0; r < nb; ++r) {
@@ -704,14 +796,10 @@ int ppmlr_gpu_harness_create(const ppmlr_axis_spec specs[3], int px, int py, int
         if (int e = ppmlr_gpu_block_set_stream(b, h->stream))
           throw SpecError(e, ppmlr_gpu_last_error());
       }
-      if (h->o.with_dipole) block_dipole(host_block(h->ax, p, g), h->o.mu0, h->bd[r]);
-      // make_block's default state {1, 0, 0, 1}
-      std::vector<double> f(h->cells(r) * 8, 0.0);
-      for (size_t c = 0; c < h->cells(r); ++c) {
-        f[8 * c] = 1.0;
-        f[8 * c + 7] = 1.0;
-      }
-      if (int e = upload_block(h, (int)r, f)) throw SpecError(e, ppmlr_gpu_last_error());
+      // make_block's default state {1, 0, 0, 1} and its dipole
+      ChunkInit ci;
+      ci.kind = -2;
+      upload_init(h, (int)r, ci, true);
     }
     return 0;
   });
@@ -734,11 +822,10 @@ int ppmlr_gpu_harness_init_magnetosphere(ppmlr_gpu_harness* h, double rho_core, 
                                          double falloff, double r_ref) {
   return guarded([&] {
     for (size_t r = 0; r < h->blocks.size(); ++r) {
-      const HostBlock hb = host_block(h->ax, h->plan[r], h->g());
-      std::vector<double> f;
-      block_magnetosphere(hb, h->o, h->bd[r], rho_core, p_core, falloff, r_ref, f, h->fidx[r],
-                          h->fst[r]);
-      if (int e = upload_block(h, (int)r, f)) throw SpecError(e, ppmlr_gpu_last_error());
+      ChunkInit ci;
+      ci.kind = -1;
+      ci.mp = {rho_core, p_core, falloff, r_ref};
+      upload_init(h, (int)r, ci, false);
     }
     return 0;
   });
@@ -747,12 +834,10 @@ int ppmlr_gpu_harness_init_magnetosphere(ppmlr_gpu_harness* h, double rho_core, 
 int ppmlr_gpu_harness_init_ic(ppmlr_gpu_harness* h, int kind, const double* params) {
   return guarded([&] {
     for (size_t r = 0; r < h->blocks.size(); ++r) {
-      const HostBlock hb = host_block(h->ax, h->plan[r], h->g());
-      std::vector<double> f;
-      block_ic(hb, kind, params, f);
-      h->fidx[r].clear();
-      h->fst[r].clear();
-      if (int e = upload_block(h, (int)r, f)) throw SpecError(e, ppmlr_gpu_last_error());
+      ChunkInit ci;
+      ci.kind = kind;
+      ci.ic = ic_of(kind, params);
+      upload_init(h, (int)r, ci, false);
     }
     return 0;
   });
@@ -762,11 +847,11 @@ int ppmlr_gpu_harness_set_state(ppmlr_gpu_harness* h, const double* all) {
   return guarded([&] {
     size_t off = 0;
     for (size_t r = 0; r < h->blocks.size(); ++r) {
-      std::vector<double> f(all + off, all + off + h->cells(r) * 8);
-      off += h->cells(r) * 8;
       h->fidx[r].clear();
       h->fst[r].clear();
-      if (int e = upload_block(h, (int)r, f)) throw SpecError(e, ppmlr_gpu_last_error());
+      if (int e = ppmlr_gpu_block_upload(h->blocks[r], all + off, nullptr, nullptr, nullptr, 0))
+        throw SpecError(e, ppmlr_gpu_last_error());
+      off += h->cells(r) * 8;
     }
     return 0;
   });
@@ -891,7 +976,11 @@ int ppmlr_gpu_harness_block_geometry(ppmlr_gpu_harness* h, int rank, int* n, int
       std::copy(h->spc[a][rank].begin(), h->spc[a][rank].end(), spacings_cat + off);
     off += h->cen[a][rank].size();
   }
-  if (bd && h->o.with_dipole) std::copy(h->bd[rank].begin(), h->bd[rank].end(), bd);
+  if (bd && h->o.with_dipole) {
+    std::vector<double> bdv;
+    block_dipole(host_block(h->ax, p, h->g()), h->o.mu0, bdv);
+    std::copy(bdv.begin(), bdv.end(), bd);
+  }
   return 0;
 }
 
