@@ -9,7 +9,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libppmlr_b200.so")
+# PPMLR_LIB selects a tuning variant built by tools/variants.py (same ABI).
+LIB_PATH = os.environ.get("PPMLR_LIB") or os.path.join(_HERE, "libppmlr_b200.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

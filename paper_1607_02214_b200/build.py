@@ -51,31 +51,33 @@ def _deps():
         os.path.join(ROOT, "include", "ppmlr_gpu.h"), __file__]
 
 
-def build_native(force=False, verbose_ptxas=False):
-    os.makedirs(OBJ, exist_ok=True)
+def build_native(force=False, verbose_ptxas=False, defines=(), out=OUT, objdir=OBJ):
+    """Compile and link the native library; `defines` / `out` / `objdir`
+    build tuning variants side by side (tools/variants.py)."""
+    os.makedirs(objdir, exist_ok=True)
     deps = _deps()
     objs = []
     for src, fmad, extra in UNITS:
-        o = os.path.join(OBJ, src.replace(".cu", ".o"))
+        o = os.path.join(objdir, src.replace(".cu", ".o"))
         objs.append(o)
         if force or _stale(o, deps):
             cmd = [NVCC, "-std=c++17", *ARCH, "-O3", "-lineinfo",
                    f"--fmad={'true' if fmad else 'false'}",
                    "-Xcompiler", "-fPIC,-ffp-contract=off", "-c", os.path.join(CSRC, src),
-                   "-o", o, *extra]
+                   "-o", o, *extra, *[f"-D{d}" for d in defines]]
             if verbose_ptxas:
                 cmd += ["-Xptxas", "-v"]
             _run(cmd)
     for src in HOST_UNITS:
-        o = os.path.join(OBJ, src.replace(".cpp", ".o"))
+        o = os.path.join(objdir, src.replace(".cpp", ".o"))
         objs.append(o)
         if force or _stale(o, deps):
             cuda_inc = os.path.join(os.path.dirname(os.path.dirname(NVCC)), "include")
             _run(["g++", "-std=c++20", "-O2", "-fPIC", "-ffp-contract=off",
                   f"-I{cuda_inc}", "-c", os.path.join(CSRC, src), "-o", o])
-    if force or _stale(OUT, objs):
-        _run([NVCC, *ARCH, "-shared", "-o", OUT, *objs, "-lcudart"])
-    return OUT
+    if force or _stale(out, objs):
+        _run([NVCC, *ARCH, "-shared", "-o", out, *objs, "-lcudart"])
+    return out
 
 
 def build_oracle():

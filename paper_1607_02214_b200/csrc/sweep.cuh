@@ -36,6 +36,12 @@ namespace ppmlr_b200 {
 // Compile-time tile length of the main sweep instantiation (L = 64 interior
 // cells per segment, 4 pencils per tile).
 constexpr int kSweepTL = 72;
+#ifndef PPMLR_SWEEP_MINB
+#define PPMLR_SWEEP_MINB 3  // resident CTAs per SM the register budget targets
+#endif
+#ifndef PPMLR_SWEEP_CSLOPE
+#define PPMLR_SWEEP_CSLOPE 1  // conserved slopes once per cell (P7b) vs per moving edge
+#endif
 
 struct SweepArgs {
   const double* src[8];  // field planes of the input buffer (padded block layout)
@@ -309,11 +315,29 @@ __device__ __forceinline__ bool sweep_tile(const SweepArgs& A, const int bid, do
                                      kErrLagUnphysical));
     }
   }
+  const bool e8 = live && s >= 4 && s <= TLv - 4;
+#if PPMLR_SWEEP_CSLOPE
+  // ---- P7b: conserved slopes at s in [1, TLv-2] -> SA (fluxes are dead) --
+  // Only tiles with a moving edge remap anything; the decision is uniform
+  // across the CTA, so the extra barrier is legal.
+  if (__syncthreads_or(e8 && CF[ci] * dt != 0.0)) {
+    if (live && s >= 1 && s <= TLv - 2) {
+      const double* gc = A.slope + 3 * q;
+      const double c0 = __ldg(gc), cA = __ldg(gc + 1), cB = __ldg(gc + 2);
+#pragma unroll
+      for (int v = 0; v < 8; ++v) {
+        const double* cv = CONS + v * T + ci;
+        SA[v * T + ci] = limited_slope(cv[-SS], cv[0], cv[SS], c0, cA, cB);
+      }
+    }
+    __syncthreads();
+  }
+#else
   __syncthreads();
+#endif
 
   // ---- P8: slivers at edges [4, TLv-4] (moving edges only) ---------------
   double sl[8];
-  const bool e8 = live && s >= 4 && s <= TLv - 4;
   if (e8) {
     const double delta = CF[ci] * dt;
 #pragma unroll
@@ -323,9 +347,12 @@ __device__ __forceinline__ bool sweep_tile(const SweepArgs& A, const int bid, do
       const int kc = right ? ci - SS : ci;  // upwind zone
       const int kq = right ? q - 1 : q;
       const double width = __ldg(A.dx + kq) + dt * (CF[kc + SS] - CF[kc]);
-      double sc[9], e0[5], e1[5];
+      double e0[5], e1[5];
+#if !PPMLR_SWEEP_CSLOPE
+      double sc[9];
 #pragma unroll
       for (int j = 0; j < 9; ++j) sc[j] = __ldg(A.slope + 3 * (kq - 1) + j);
+#endif
 #pragma unroll
       for (int j = 0; j < 5; ++j) {
         e0[j] = __ldg(A.qfc + 5 * kq + j);
@@ -340,7 +367,13 @@ __device__ __forceinline__ bool sweep_tile(const SweepArgs& A, const int bid, do
         const double* cv = CONS + v * T + kc;
         auto win = [&](int j) { return cv[j * SS]; };
         double al, ar, six;
+#if PPMLR_SWEEP_CSLOPE
+        const double* dv = SA + v * T + kc;
+        auto dwin = [&](int j) { return dv[j * SS]; };
+        zone_parabola_dm(win, dwin, e0, e1, k, o, al, ar, six);
+#else
         zone_parabola(win, sc, e0, e1, k, o, al, ar, six);
+#endif
         const double mean =
             right ? avg_right(al, ar, six, hs, tw) : avg_left(al, ar, six, hs, tw);
         sl[v] = delta * (mean + (PRIM[v * T + kc] - cv[0]));
@@ -400,7 +433,7 @@ using MainOps = FastOps;      // bit-exact replay of nvcc's fast paths
 // commits its error keys and results, otherwise it is queued for EXACT,
 // which re-runs the queued tiles with plain `/` and `sqrt`.
 template <int AXIS, bool DIPOLE, int NP, int TLC, bool EXACT>
-__global__ void __launch_bounds__(NP * kSweepTL, 3) sweep_kernel(const SweepArgs A) {
+__global__ void __launch_bounds__(NP * kSweepTL, PPMLR_SWEEP_MINB) sweep_kernel(const SweepArgs A) {
   extern __shared__ double smem[];
   __shared__ unsigned long long s_err;
   if (EXACT) {
