@@ -488,6 +488,10 @@ int launch_sweep(ppmlr_gpu_block* b, int axis, int phase) {
   A.L = b->sweep_L[axis];
   A.nseg = (A.n + A.L - 1) / A.L;
   A.ngroups = (A.ng + 3) / 4;
+  if (A.ngroups > 65535 || A.no > 65535) {  // grid (nseg, ngroups, no)
+    set_error("sweep: too many pencils across the sweep axis for one launch grid");
+    return PPMLR_INVALID_SPEC;
+  }
   A.dt = b->d_dt;
   A.err = b->d_err;
   A.step = b->d_step;
@@ -719,6 +723,20 @@ int ppmlr_gpu_block_create(const ppmlr_gpu_block_desc* d, ppmlr_gpu_block** out)
       set_error("rcp_table_kernel failed");
       return fail(PPMLR_RUNTIME);
     }
+  }
+  {  // reciprocals of the run constants, refined on the device once
+    std::vector<double> rc5 = {b->c.gm1, b->c.two_mu0, b->c.mu0, 6.0, 3.0};
+    double* d5 = nullptr;
+    if ((rc = upload_vec(&d5, rc5))) return fail(rc);
+    rcp_table_kernel<<<1, 32>>>(d5, 5);
+    const cudaError_t e5 = cudaMemcpy(rc5.data(), d5, 5 * sizeof(double), cudaMemcpyDeviceToHost);
+    cudaFree(d5);
+    if (e5 != cudaSuccess) return fail(cuda_fail(e5, "constant reciprocals"));
+    b->c.r_gm1 = rc5[0];
+    b->c.r_two_mu0 = rc5[1];
+    b->c.r_mu0 = rc5[2];
+    b->c.r6 = rc5[3];
+    b->c.r3 = rc5[4];
   }
   cudaError_t e;
   for (int k = 0; k < 2; ++k) {

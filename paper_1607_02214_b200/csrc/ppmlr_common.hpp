@@ -17,6 +17,9 @@ struct Consts {
   double gamma, mu0, pressure_floor;
   double gm1;      // gamma - 1.0   (hoisted; same rounding as the reference's inline form)
   double two_mu0;  // 2.0 * mu0     (hoisted; exact)
+  // rcp_refined of gm1, two_mu0, mu0, 6 and 3 (the divisor-only half of
+  // nvcc's `/`), computed once on the device when the block is created
+  double r_gm1, r_two_mu0, r_mu0, r6, r3;
 };
 
 // Strip-frame variable slots (proj/include/ppmlr/ppm1d.hpp:50).

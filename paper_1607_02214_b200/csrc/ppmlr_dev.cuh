@@ -19,8 +19,8 @@ namespace ppmlr_b200 {
 
 namespace PPMLR_KNS {
 
-// Reciprocals of the run constants and of the literal divisors 6 and 3,
-// refined once per thread (the divisor-only half of nvcc's `/`).
+// Reciprocals of the run constants and of the literal divisors 6 and 3
+// (precomputed per block with rcp_refined; see Consts).
 struct KC {
   Consts c;
   double r_gm1, r_two_mu0, r_mu0, r6, r3;
@@ -28,11 +28,11 @@ struct KC {
 __device__ __forceinline__ KC make_kc(const Consts& c) {
   KC k;
   k.c = c;
-  k.r_gm1 = rcp_refined(c.gm1);
-  k.r_two_mu0 = rcp_refined(c.two_mu0);
-  k.r_mu0 = rcp_refined(c.mu0);
-  k.r6 = rcp_refined(6.0);
-  k.r3 = rcp_refined(3.0);
+  k.r_gm1 = c.r_gm1;
+  k.r_two_mu0 = c.r_two_mu0;
+  k.r_mu0 = c.r_mu0;
+  k.r6 = c.r6;
+  k.r3 = c.r3;
   return k;
 }
 

@@ -11,12 +11,13 @@
 //   P0  load; strip-frame prim, cons, c_f                      -> PRIM, CONS, CF
 //   P1  primitive slopes (once per cell)                        -> SA
 //   P3  per zone: interface values, limited parabola, traced
-//       edge states (written after a barrier)                   -> PRIM:=R, SA:=L
+//       edge states, in two halves of four variables (each
+//       written after a barrier)                                -> PRIM:=R, SA:=L
 //   P4  per edge: Lagrangian Riemann solve                      -> CF:=u*, SA:=flux
 //   P7  per zone: Lagrangian update + the reference's checks    -> PRIM:=lag
+//   P7b tiles with a moving edge: conserved slopes per cell     -> SA
 //   P8  per moving edge only: the upwind zone's conserved
-//       parabola (5-point window) and the remap sliver
-//       (written after a barrier)                               -> CONS:=sliver
+//       parabola and the remap sliver (written after a barrier) -> CONS:=sliver
 //   P9  per zone: remap onto the fixed mesh, cons_to_prim, store
 //
 // 25 shared FP64 slots per cell (+3 with the dipole): 57.6 KB for the 288-cell
@@ -83,6 +84,15 @@ struct AxisMap {
   static constexpr int B = (AXIS + 1) % 3;  // reference t1 axis
 };
 
+// Tile coordinates: segment along AXIS, group of NP pencils, other axis.
+struct TileId {
+  int seg, grp, oc;
+};
+__device__ __forceinline__ TileId tile_of(const SweepArgs& A, int t) {
+  const int rest = t / A.nseg;
+  return {t - rest * A.nseg, rest % A.ngroups, rest / A.ngroups};
+}
+
 // The limited parabola of zone (tile row s) from the 5-point window of one
 // variable: reconstruct() (ppm1d.cpp:200-247) restricted to one zone.
 template <class W, class Ops>
@@ -110,8 +120,9 @@ __device__ __forceinline__ void zone_parabola_dm(const W& q, const D& dm, const 
 }
 
 template <int AXIS, bool DIPOLE, int NP, int TLC, class Ops>
-__device__ __forceinline__ bool sweep_tile(const SweepArgs& A, const int bid, double* smem,
-                                              unsigned long long* s_err) {
+__device__ __forceinline__ bool sweep_tile(const SweepArgs& A, const int seg, const int grp,
+                                           const int oc, double* smem,
+                                           unsigned long long* s_err) {
   bool tbad = false;
   const int TL = TLC > 0 ? TLC : A.L + 8;
   const int T = NP * TL;
@@ -122,10 +133,6 @@ __device__ __forceinline__ bool sweep_tile(const SweepArgs& A, const int bid, do
   double* BD = smem + 25 * T;
   const int SS = AXIS == 0 ? 1 : NP;
 
-  const int seg = bid % A.nseg;
-  const int rest = bid / A.nseg;
-  const int grp = rest % A.ngroups;
-  const int oc = rest / A.ngroups;
   const int nn = A.n + 8;
   const int seg0 = seg * A.L;
   const int TLv = min(TL, nn - seg0);
@@ -213,11 +220,16 @@ __device__ __forceinline__ bool sweep_tile(const SweepArgs& A, const int bid, do
   __syncthreads();
 
   // ---- P3: prim parabolas -> traced states (zones [2, zmax]) ------------
-  double L[8], R[8];
+  // Two halves of four variables, each written back after a barrier, so
+  // that only eight traced values are held across a barrier.  The first
+  // half holds rho and p, which decide the reference's fallback to the
+  // zone's own state for all eight.
   const bool z3 = live && s >= 2 && s <= zmax;
+  const bool flat = q >= nn - 2;  // q >= 2 always here
+  double e0[5], e1[5], hs = 0.0, tw = 0.0;
+  bool badL = false, badR = false;
+  Ops o3;
   if (z3) {
-    const bool flat = q >= nn - 2;  // q >= 2 always here
-    double e0[5], e1[5];
     if (!flat) {
 #pragma unroll
       for (int j = 0; j < 5; ++j) {
@@ -225,41 +237,73 @@ __device__ __forceinline__ bool sweep_tile(const SweepArgs& A, const int bid, do
         e1[j] = __ldg(A.qfc + 5 * (q + 1) + j);
       }
     }
-    Ops o;
     const double sigma =
-        sclamp(o.div(CF[ci] * dt, __ldg(A.dx + q), __ldg(A.rdx + q)), 0.0, 1.0);
-    const double hs = 0.5 * sigma;
-    const double tw = tw_of(sigma, k, o);
-#pragma unroll
-    for (int v = 0; v < 8; ++v) {
-      const double* pv = PRIM + v * T + ci;
-      const double av = pv[0];
-      double al = av, ar = av, six = 0.0;
-      if (!flat) {
-        const double* dv = SA + v * T + ci;
-        auto win = [&](int j) { return pv[j * SS]; };
-        auto dwin = [&](int j) { return dv[j * SS]; };
-        zone_parabola_dm(win, dwin, e0, e1, k, o, al, ar, six);
-      }
-      L[v] = avg_left(al, ar, six, hs, tw);
-      R[v] = avg_right(al, ar, six, hs, tw);
+        sclamp(o3.div(CF[ci] * dt, __ldg(A.dx + q), __ldg(A.rdx + q)), 0.0, 1.0);
+    hs = 0.5 * sigma;
+    tw = tw_of(sigma, k, o3);
+  }
+  auto trace = [&](const int v, double& l, double& r) {
+    const double* pv = PRIM + v * T + ci;
+    const double av = pv[0];
+    double al = av, ar = av, six = 0.0;
+    if (!flat) {
+      const double* dv = SA + v * T + ci;
+      auto win = [&](int j) { return pv[j * SS]; };
+      auto dwin = [&](int j) { return dv[j * SS]; };
+      zone_parabola_dm(win, dwin, e0, e1, k, o3, al, ar, six);
     }
-    tbad |= o.bad;
-    const bool badL = !(L[kRho] > 0.0) || !(L[kPE] > 0.0);
-    const bool badR = !(R[kRho] > 0.0) || !(R[kPE] > 0.0);
+    l = avg_left(al, ar, six, hs, tw);
+    r = avg_right(al, ar, six, hs, tw);
+  };
+  {
+    const int H[4] = {kRho, kPE, kUn, kUt1};
+    double L[4], R[4];
+    if (z3) {
 #pragma unroll
-    for (int v = 0; v < 8; ++v) {
-      const double own = PRIM[v * T + ci];
-      if (badL) L[v] = own;
-      if (badR) R[v] = own;
+      for (int j = 0; j < 4; ++j) trace(H[j], L[j], R[j]);
+      badL = !(L[0] > 0.0) || !(L[1] > 0.0);
+      badR = !(R[0] > 0.0) || !(R[1] > 0.0);
+      if (badL || badR) {  // rare: the zone falls back to its own state
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const double own = PRIM[H[j] * T + ci];
+          if (badL) L[j] = own;
+          if (badR) R[j] = own;
+        }
+      }
+    }
+    __syncthreads();
+    if (z3) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        PRIM[H[j] * T + ci] = R[j];
+        SA[H[j] * T + ci] = L[j];
+      }
     }
   }
-  __syncthreads();
-  if (z3) {
+  {
+    const int H[4] = {kUt2, kBn, kBt1, kBt2};
+    double L[4], R[4];
+    if (z3) {
 #pragma unroll
-    for (int v = 0; v < 8; ++v) {
-      PRIM[v * T + ci] = R[v];
-      SA[v * T + ci] = L[v];
+      for (int j = 0; j < 4; ++j) trace(H[j], L[j], R[j]);
+      if (badL || badR) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const double own = PRIM[H[j] * T + ci];
+          if (badL) L[j] = own;
+          if (badR) R[j] = own;
+        }
+      }
+      tbad |= o3.bad;
+    }
+    __syncthreads();
+    if (z3) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        PRIM[H[j] * T + ci] = R[j];
+        SA[H[j] * T + ci] = L[j];
+      }
     }
   }
   __syncthreads();
@@ -429,6 +473,7 @@ using MainOps = FastMathOps;  // tolerance-gated fast mode
 using MainOps = FastOps;      // bit-exact replay of nvcc's fast paths
 #endif
 
+
 // Main instance: every tile with MainOps; a tile whose guards all held
 // commits its error keys and results, otherwise it is queued for EXACT,
 // which re-runs the queued tiles with plain `/` and `sqrt`.
@@ -441,7 +486,8 @@ __global__ void __launch_bounds__(NP * kSweepTL, PPMLR_SWEEP_MINB) sweep_kernel(
     for (unsigned i = blockIdx.x; i < n; i += gridDim.x) {
       if (threadIdx.x == 0) s_err = kNoError;
       __syncthreads();
-      sweep_tile<AXIS, DIPOLE, NP, TLC, ExactOps>(A, (int)A.redo_list[i], smem, &s_err);
+      const TileId id = tile_of(A, (int)A.redo_list[i]);
+      sweep_tile<AXIS, DIPOLE, NP, TLC, ExactOps>(A, id.seg, id.grp, id.oc, smem, &s_err);
       __syncthreads();
       if (threadIdx.x == 0 && s_err != kNoError) atomicMin(A.err, s_err);
       __syncthreads();
@@ -450,9 +496,13 @@ __global__ void __launch_bounds__(NP * kSweepTL, PPMLR_SWEEP_MINB) sweep_kernel(
   }
   if (threadIdx.x == 0) s_err = kNoError;
   __syncthreads();
-  const bool bad = sweep_tile<AXIS, DIPOLE, NP, TLC, MainOps>(A, blockIdx.x, smem, &s_err);
+  // grid = (nseg, ngroups, no): the tile coordinates need no division
+  const bool bad = sweep_tile<AXIS, DIPOLE, NP, TLC, MainOps>(A, blockIdx.x, blockIdx.y,
+                                                              blockIdx.z, smem, &s_err);
   if (__syncthreads_or(bad)) {
-    if (threadIdx.x == 0) A.redo_list[atomicAdd(A.redo_count, 1u)] = blockIdx.x;
+    if (threadIdx.x == 0)
+      A.redo_list[atomicAdd(A.redo_count, 1u)] =
+          blockIdx.x + A.nseg * (blockIdx.y + A.ngroups * blockIdx.z);
   } else if (threadIdx.x == 0 && s_err != kNoError) {
     atomicMin(A.err, s_err);
   }
