@@ -125,6 +125,16 @@ int ppmlr_gpu_block_upload(ppmlr_gpu_block* b, const double* fields, const doubl
 int ppmlr_gpu_block_download(ppmlr_gpu_block* b, double* fields);
 /* Device -> host: interior only, AoS x fastest (gather_interior order). */
 int ppmlr_gpu_block_download_interior(ppmlr_gpu_block* b, double* out);
+/* Snapshot of the current state (the device half of gather_interior ->
+ * write_snapshot, tools/ppmlr_main.cpp:20-31, src/snapshot.cpp:58-85):
+ * capture copies the interior, field-major and x fastest, to a device
+ * buffer in stream order and returns at once; read drains interior planes
+ * [k0, k0+nk) of one field (0..7 = rho, vx, vy, vz, B'x, B'y, B'z, p) to
+ * host memory on the block's snapshot stream, row pitch / plane slice in
+ * doubles, so a caller can place the block inside a global array. */
+int ppmlr_gpu_block_snapshot_capture(ppmlr_gpu_block* b);
+int ppmlr_gpu_block_snapshot_read(ppmlr_gpu_block* b, int field, int k0, int nk, double* dst,
+                                  int64_t dst_pitch, int64_t dst_slice);
 
 /* compute_dt (stepper.cpp:119-139): cfl * min over the block. */
 int ppmlr_gpu_block_compute_dt(ppmlr_gpu_block* b, double cfl, double* dt_out);
@@ -252,6 +262,21 @@ ppmlr_gpu_block* ppmlr_gpu_harness_block(ppmlr_gpu_harness* h, int rank);
 /* TransferLedger totals (exchange.hpp:48-61): bytes, messages, copy events. */
 void ppmlr_gpu_harness_ledger(ppmlr_gpu_harness* h, uint64_t* bytes, long* messages,
                               long* copy_events);
+/* TransferLedger entries (one per exchange_step, exchange.cpp:93-149):
+ * returns the count and fills at most `max` of each array (any may be NULL).
+ * transport: 0 staged, 1 direct. */
+long ppmlr_gpu_harness_ledger_entries(ppmlr_gpu_harness* h, long* step, int* transport,
+                                      long* messages, uint64_t* bytes, long* copy_events,
+                                      long max);
+/* write_snapshot(path, make_snapshot(h)) (src/snapshot.cpp:58-85,
+ * tools/ppmlr_main.cpp:20-31): the PPLR v1 file of the current state.
+ * _begin captures the state on the device and returns; a host thread drains
+ * it to the file while the caller keeps stepping.  _wait joins and returns
+ * the writer's status (InvalidSpec "snapshot: cannot open for writing: ..."
+ * like the reference).  ppmlr_gpu_harness_snapshot = begin + wait. */
+int ppmlr_gpu_harness_snapshot_begin(ppmlr_gpu_harness* h, const char* path);
+int ppmlr_gpu_harness_snapshot_wait(ppmlr_gpu_harness* h);
+int ppmlr_gpu_harness_snapshot(ppmlr_gpu_harness* h, const char* path);
 /* Frozen-core record of block r (count if idx == NULL). */
 int64_t ppmlr_gpu_harness_frozen(ppmlr_gpu_harness* h, int rank, int64_t* idx,
                                  double* states);

@@ -256,6 +256,9 @@ def ref():
         lib.ref_harness_ledger_messages.restype = C.c_long
         lib.ref_harness_ledger_copy_events.argtypes = [vp]
         lib.ref_harness_ledger_copy_events.restype = C.c_long
+        lib.ref_harness_ledger_entries.argtypes = [vp] + [C.c_void_p] * 5 + [C.c_long]
+        lib.ref_harness_ledger_entries.restype = C.c_long
+        lib.ref_harness_write_snapshot.argtypes = [vp, C.c_char_p, C.c_char_p, C.c_int]
         lib.ref_bench.argtypes = [C.POINTER(RefAxisSpec), C.POINTER(RefOptions), C.c_int, _dp,
                                   C.c_int, C.c_int, _dp, _dp, C.c_char_p, C.c_int]
         _ref = lib
@@ -414,6 +417,21 @@ class RefHarness:
     def ledger(self):
         return (ref().ref_harness_ledger_bytes(self.h), ref().ref_harness_ledger_messages(self.h),
                 ref().ref_harness_ledger_copy_events(self.h))
+
+    def ledger_csv(self):
+        """TransferLedger::to_csv (exchange.cpp:84-91) of the reference's entries."""
+        n = ref().ref_harness_ledger_entries(self.h, None, None, None, None, None, 0)
+        st, tr, ms = (C.c_long * n)(), (C.c_int * n)(), (C.c_long * n)()
+        by, ev = (C.c_uint64 * n)(), (C.c_long * n)()
+        ref().ref_harness_ledger_entries(self.h, st, tr, ms, by, ev, n)
+        rows = ["step,transport,messages,bytes,copy_events"]
+        rows += [f"{st[i]},{'direct' if tr[i] else 'staged'},{ms[i]},{by[i]},{ev[i]}"
+                 for i in range(n)]
+        return "\n".join(rows) + "\n"
+
+    def write_snapshot(self, path):
+        err = C.create_string_buffer(512)
+        self._chk(ref().ref_harness_write_snapshot(self.h, os.fsencode(path), err, 512), err)
 
 
 def ref_bench(specs, ic_kind, ic_params, threads, steps, **kw):

@@ -16,6 +16,7 @@
 #include "ppmlr/errors.hpp"
 #include "ppmlr/grid.hpp"
 #include "ppmlr/harness.hpp"
+#include "ppmlr/snapshot.hpp"
 #include "ppmlr/ppm1d.hpp"
 #include "ppmlr/stepper.hpp"
 
@@ -362,6 +363,42 @@ double ref_harness_time(void* h) { return H(h).time(); }
 uint64_t ref_harness_ledger_bytes(void* h) { return H(h).ledger().total_bytes; }
 long ref_harness_ledger_messages(void* h) { return H(h).ledger().total_messages; }
 long ref_harness_ledger_copy_events(void* h) { return H(h).ledger().total_copy_events; }
+
+// The reference's ledger entries (TransferLedger::entries, exchange.hpp:40-61);
+// returns the count, fills at most `max`.  (The CSV text is formatted by the
+// caller: ostream number formatting inside a ctypes-loaded library crashed
+// in the Python test process.)
+long ref_harness_ledger_entries(void* h, long* step, int* transport, long* messages,
+                                uint64_t* bytes, long* copy_events, long max) {
+  const auto& e = H(h).ledger().entries;
+  const long n = (long)e.size();
+  for (long i = 0; i < std::min(n, max); ++i) {
+    step[i] = e[i].step;
+    transport[i] = e[i].transport == TransportKind::Direct ? 1 : 0;
+    messages[i] = e[i].messages;
+    bytes[i] = e[i].bytes;
+    copy_events[i] = e[i].copy_events;
+  }
+  return n;
+}
+
+// `ppmlr run`'s snapshot of the current state: make_snapshot
+// (tools/ppmlr_main.cpp:20-31) + write_snapshot (snapshot.cpp:58-85).
+int ref_harness_write_snapshot(void* h, const char* path, char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    const Harness& hh = H(h);
+    Snapshot s;
+    const StretchedGrid& g = hh.grid();
+    s.dims = {static_cast<std::uint32_t>(g.x.n()), static_cast<std::uint32_t>(g.y.n()),
+              static_cast<std::uint32_t>(g.z.n())};
+    s.ghost = static_cast<std::uint32_t>(hh.options().ghost);
+    s.time = hh.time();
+    s.step = static_cast<std::uint64_t>(hh.step_count());
+    for (int a = 0; a < 3; ++a) s.edges[a] = g.axis(a).edges;
+    s.fields = hh.gather_interior();
+    write_snapshot(path, s);
+  });
+}
 
 int ref_bench(const ref_axis_spec* specs3, const ref_options* opts, int ic_kind,
               const double* ic_params, int threads, int steps, double* rate,

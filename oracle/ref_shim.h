@@ -84,6 +84,9 @@ double ref_harness_time(void* h);
 uint64_t ref_harness_ledger_bytes(void* h);
 long ref_harness_ledger_messages(void* h);
 long ref_harness_ledger_copy_events(void* h);
+long ref_harness_ledger_entries(void* h, long* step, int* transport, long* messages,
+                                uint64_t* bytes, long* copy_events, long max);
+int ref_harness_write_snapshot(void* h, const char* path, char* err, int errlen);
 
 /* CPU baseline: `threads` independent harnesses (one per thread) built from
  * the same spec and IC, each advanced `steps` times.  Returns aggregate

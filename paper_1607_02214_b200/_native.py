@@ -118,6 +118,9 @@ _sig("ppmlr_gpu_block_destroy", None, _BP)
 _sig("ppmlr_gpu_block_upload", C.c_int, _BP, _dp, _dp, _i64p, _dp, C.c_int64)
 _sig("ppmlr_gpu_block_download", C.c_int, _BP, _dp)
 _sig("ppmlr_gpu_block_download_interior", C.c_int, _BP, _dp)
+_sig("ppmlr_gpu_block_snapshot_capture", C.c_int, _BP)
+_sig("ppmlr_gpu_block_snapshot_read", C.c_int, _BP, C.c_int, C.c_int, C.c_int, _dp, C.c_int64,
+     C.c_int64)
 _sig("ppmlr_gpu_block_compute_dt", C.c_int, _BP, C.c_double, _dp)
 _sig("ppmlr_gpu_block_fill_boundaries", C.c_int, _BP, C.c_int, C.c_int)
 _sig("ppmlr_gpu_block_sweep", C.c_int, _BP, C.c_int, C.c_double)
@@ -159,6 +162,12 @@ _sig("ppmlr_gpu_harness_block", _vp, _vp, C.c_int)
 _sig("ppmlr_gpu_harness_ledger", None, _vp, C.POINTER(C.c_uint64), C.POINTER(C.c_long),
      C.POINTER(C.c_long))
 _sig("ppmlr_gpu_harness_frozen", C.c_int64, _vp, C.c_int, _i64p, _dp)
+_sig("ppmlr_gpu_harness_ledger_entries", C.c_long, _vp, C.POINTER(C.c_long),
+     C.POINTER(C.c_int), C.POINTER(C.c_long), C.POINTER(C.c_uint64), C.POINTER(C.c_long),
+     C.c_long)
+_sig("ppmlr_gpu_harness_snapshot_begin", C.c_int, _vp, C.c_char_p)
+_sig("ppmlr_gpu_harness_snapshot_wait", C.c_int, _vp)
+_sig("ppmlr_gpu_harness_snapshot", C.c_int, _vp, C.c_char_p)
 _sig("ppmlr_gpu_harness_block_geometry", C.c_int, _vp, C.c_int, _ip, _ip, _dp, _dp, _dp)
 
 

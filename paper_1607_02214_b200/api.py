@@ -9,6 +9,7 @@ Names, argument meaning and error behaviour follow the reference
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -304,6 +305,36 @@ class Harness:
         b, m, e = C.c_uint64(), C.c_long(), C.c_long()
         N.lib.ppmlr_gpu_harness_ledger(self.h, C.byref(b), C.byref(m), C.byref(e))
         return int(b.value), int(m.value), int(e.value)
+
+    def ledger_entries(self):
+        """TransferLedger.entries (exchange.hpp:40-61): one row per
+        exchange_step as (step, transport, messages, bytes, copy_events)."""
+        n = N.lib.ppmlr_gpu_harness_ledger_entries(self.h, None, None, None, None, None, 0)
+        st, tr, ms = (C.c_long * n)(), (C.c_int * n)(), (C.c_long * n)()
+        by, ev = (C.c_uint64 * n)(), (C.c_long * n)()
+        N.lib.ppmlr_gpu_harness_ledger_entries(self.h, st, tr, ms, by, ev, n)
+        return [(int(st[i]), "direct" if tr[i] else "staged", int(ms[i]), int(by[i]),
+                 int(ev[i])) for i in range(n)]
+
+    def ledger_csv(self):
+        """TransferLedger::to_csv (exchange.cpp:84-91)."""
+        rows = ["step,transport,messages,bytes,copy_events"]
+        rows += [",".join(str(x) for x in e) for e in self.ledger_entries()]
+        return "\n".join(rows) + "\n"
+
+    def write_snapshot(self, path, wait=True):
+        """write_snapshot(path, make_snapshot(h)) (snapshot.cpp:58-85,
+        ppmlr_main.cpp:20-31).  With wait=False the state is captured on the
+        device and the file is written by a host thread while stepping goes
+        on; snapshot_wait() (or the next snapshot) joins it."""
+        p = os.fsencode(path)
+        if wait:
+            check(N.lib.ppmlr_gpu_harness_snapshot(self.h, p))
+        else:
+            check(N.lib.ppmlr_gpu_harness_snapshot_begin(self.h, p))
+
+    def snapshot_wait(self):
+        check(N.lib.ppmlr_gpu_harness_snapshot_wait(self.h))
 
     def frozen(self, rank=0):
         k = N.lib.ppmlr_gpu_harness_frozen(self.h, rank, None, None)

@@ -114,6 +114,21 @@ __global__ void soa_to_aos_kernel(double* __restrict__ aos, Planes src, Lay L, i
 }
 
 // Interior only, x fastest.
+// Interior of every field plane, field-major, x fastest (the PPLR payload
+// order, snapshot.cpp:78-83): out[f * cells + i + n0 * (j + n1 * k)].
+__global__ void interior_planes_kernel(double* __restrict__ out, Planes src, Lay L) {
+  const long long total = (long long)L.n0 * L.n1 * L.n2;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(t % L.n0);
+    const int j = (int)((t / L.n0) % L.n1);
+    const int k = (int)(t / ((long long)L.n0 * L.n1));
+    const long long d = L.idx(i, j, k);
+#pragma unroll
+    for (int f = 0; f < 8; ++f) out[f * total + t] = src.f[f][d];
+  }
+}
+
 __global__ void soa_to_interior_kernel(double* __restrict__ out, Planes src, Lay L) {
   const long long total = (long long)L.n0 * L.n1 * L.n2;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
@@ -801,6 +816,10 @@ void ppmlr_gpu_block_destroy(ppmlr_gpu_block* b) {
     cudaFree(b->ax[a].den);
     cudaFree(b->ax[a].rden);
   }
+  if (b->snap_stream) cudaStreamSynchronize(b->snap_stream);
+  cudaFree(b->d_snap);
+  if (b->snap_stream) cudaStreamDestroy(b->snap_stream);
+  if (b->snap_ready) cudaEventDestroy(b->snap_ready);
   cudaFree(b->fslot);
   cudaFree(b->fstates);
   cudaFree(b->fidx);
@@ -1011,6 +1030,44 @@ int ppmlr_gpu_block_download(ppmlr_gpu_block* b, double* fields) {
 }
 int ppmlr_gpu_block_download_interior(ppmlr_gpu_block* b, double* out) {
   return download_impl(b, out, true);
+}
+
+int ppmlr_gpu_block_snapshot_capture(ppmlr_gpu_block* b) {
+  CK(cudaSetDevice(b->device));
+  const long long cells = (long long)b->n[0] * b->n[1] * b->n[2];
+  if (!b->snap_stream) {
+    CK(cudaStreamCreateWithFlags(&b->snap_stream, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&b->snap_ready, cudaEventDisableTiming));
+  }
+  // the previous capture must be fully drained before it is overwritten
+  CK(cudaStreamSynchronize(b->snap_stream));
+  if (!b->d_snap) CK(cudaMalloc(&b->d_snap, sizeof(double) * 8 * (size_t)cells));
+  interior_planes_kernel<<<grid_for(cells), 256, 0, b->stream>>>(
+      b->d_snap, planes(cur_buf(b), b->ncell), lay_of(b));
+  CK(cudaGetLastError());
+  b->kernel_launches += 1;
+  CK(cudaEventRecord(b->snap_ready, b->stream));
+  return 0;
+}
+
+int ppmlr_gpu_block_snapshot_read(ppmlr_gpu_block* b, int field, int k0, int nk, double* dst,
+                                  int64_t dst_pitch, int64_t dst_slice) {
+  CK(cudaSetDevice(b->device));
+  if (!b->d_snap || field < 0 || field > 7 || k0 < 0 || nk < 0 || k0 + nk > b->n[2] ||
+      dst_pitch < b->n[0] || dst_slice < dst_pitch * b->n[1]) {
+    set_error("snapshot_read: no capture or range outside the block interior");
+    return PPMLR_INVALID_SPEC;
+  }
+  const size_t plane = (size_t)b->n[0] * b->n[1];
+  const double* src = b->d_snap + (size_t)field * plane * b->n[2];
+  CK(cudaStreamWaitEvent(b->snap_stream, b->snap_ready, 0));
+  for (int k = 0; k < nk; ++k)
+    CK(cudaMemcpy2DAsync(dst + (size_t)k * dst_slice, sizeof(double) * dst_pitch,
+                         src + (size_t)(k0 + k) * plane, sizeof(double) * b->n[0],
+                         sizeof(double) * b->n[0], b->n[1], cudaMemcpyDeviceToHost,
+                         b->snap_stream));
+  CK(cudaStreamSynchronize(b->snap_stream));
+  return 0;
 }
 
 int ppmlr_gpu_block_check(ppmlr_gpu_block* b) {

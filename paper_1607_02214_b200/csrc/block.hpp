@@ -93,6 +93,12 @@ struct ppmlr_gpu_block {
   long kernel_launches = 0;              // every kernel this block enqueued
   int sweep_L[3] = {0, 0, 0};            // segment length per axis
   int sweep_threads[3] = {0, 0, 0};
+  // snapshot (gather_interior -> write_snapshot): a device copy of the
+  // interior, field-major and x fastest like the PPLR payload, drained to
+  // the host on its own stream while stepping continues
+  double* d_snap = nullptr;
+  cudaStream_t snap_stream = nullptr;
+  cudaEvent_t snap_ready = nullptr;
 };
 
 namespace ppmlr_b200 {

@@ -542,6 +542,14 @@ HostBlock host_block(const Axis* ax, const BlockPlan& p, int g) {
 
 // ------------------------------------------------------------- harness
 
+struct LedgerRow {  // LedgerEntry (exchange.hpp:40-46)
+  long step;
+  int transport;  // 0 staged, 1 direct
+  long messages;
+  uint64_t bytes;
+  long copy_events;
+};
+
 struct ppmlr_gpu_harness {
   Axis ax[3];
   int cnt[3] = {1, 1, 1};
@@ -557,6 +565,10 @@ struct ppmlr_gpu_harness {
   cudaStream_t stream = nullptr;  // one stream orders every block's work
   uint64_t ledger_bytes = 0;
   long ledger_messages = 0, ledger_events = 0;
+  std::vector<LedgerRow> ledger;
+  std::thread snap_writer;  // drains the last snapshot capture to its file
+  int snap_rc = 0;
+  std::string snap_err;
 
   int g() const { return o.ghost; }
   size_t cells(int r) const {
@@ -592,17 +604,22 @@ void upload_init(ppmlr_gpu_harness* h, int r, ChunkInit ci, bool with_bd) {
 
 // Ledger entry of one exchange_step (exchange.cpp:93-149): every interior
 // face both ways, payload face_cells*ghost*8 doubles; staged adds 6 copies.
-void record_exchange(ppmlr_gpu_harness* h) {
+void record_exchange(ppmlr_gpu_harness* h, long step) {
+  LedgerRow e{step, h->o.transport, 0, 0, 0};
   for (const BlockPlan& b : h->plan)
     for (int face = 0; face < 6; ++face) {
       if (b.neighbor[face] < 0) continue;
       const int a = face / 2;
       const uint64_t payload =
           (uint64_t)b.n[(a + 1) % 3] * b.n[(a + 2) % 3] * h->g() * 8 * sizeof(double);
-      h->ledger_messages += 1;
-      h->ledger_bytes += payload;
-      h->ledger_events += 1 + (h->o.transport == 0 ? 6 : 0);
+      e.messages += 1;
+      e.bytes += payload;
+      e.copy_events += 1 + (h->o.transport == 0 ? 6 : 0);
     }
+  h->ledger.push_back(e);
+  h->ledger_messages += e.messages;
+  h->ledger_bytes += e.bytes;
+  h->ledger_events += e.copy_events;
 }
 
 // exchange_and_fill (harness.cpp:52-57): halos from neighbours, then
@@ -614,7 +631,7 @@ int exchange_and_fill(ppmlr_gpu_harness* h) {
       if (nb < 0) continue;
       if (int rc = ppmlr_gpu_block_copy_face(h->blocks[r], face, h->blocks[nb], kG)) return rc;
     }
-  record_exchange(h);
+  record_exchange(h, h->step);
   for (auto* b : h->blocks)
     if (int rc = ppmlr_gpu_block_fill_boundaries(b, 7, kG)) return rc;
   return 0;
@@ -813,6 +830,7 @@ int ppmlr_gpu_harness_create(const ppmlr_axis_spec specs[3], int px, int py, int
 
 void ppmlr_gpu_harness_destroy(ppmlr_gpu_harness* h) {
   if (!h) return;
+  if (h->snap_writer.joinable()) h->snap_writer.join();
   for (auto* b : h->blocks) ppmlr_gpu_block_destroy(b);
   if (h->stream) cudaStreamDestroy(h->stream);
   delete h;
@@ -877,7 +895,7 @@ int ppmlr_gpu_harness_advance(ppmlr_gpu_harness* h, double* dt_out) {
     if (int rc = ppmlr_gpu_block_advance(h->blocks[0], h->o.cfl, h->o.with_sources, h->step,
                                          &dt))
       return rc;
-    for (int e = 0; e < 3 + (h->o.with_sources ? 1 : 0); ++e) record_exchange(h);
+    for (int e = 0; e < 3 + (h->o.with_sources ? 1 : 0); ++e) record_exchange(h, h->step);
   } else {
     if (int rc = ppmlr_gpu_harness_compute_dt(h, &dt)) return rc;
     for (auto* b : h->blocks)
@@ -911,9 +929,9 @@ int ppmlr_gpu_harness_run(ppmlr_gpu_harness* h, long steps) {
                                      &t))
       return rc;
     h->time = t;
-    h->step += steps;
     for (long s = 0; s < steps; ++s)
-      for (int e = 0; e < 3 + (h->o.with_sources ? 1 : 0); ++e) record_exchange(h);
+      for (int e = 0; e < 3 + (h->o.with_sources ? 1 : 0); ++e) record_exchange(h, h->step + s);
+    h->step += steps;
     return 0;
   }
   for (long s = 0; s < steps; ++s)
@@ -951,6 +969,102 @@ void ppmlr_gpu_harness_ledger(ppmlr_gpu_harness* h, uint64_t* bytes, long* messa
   if (bytes) *bytes = h->ledger_bytes;
   if (messages) *messages = h->ledger_messages;
   if (copy_events) *copy_events = h->ledger_events;
+}
+
+long ppmlr_gpu_harness_ledger_entries(ppmlr_gpu_harness* h, long* step, int* transport,
+                                      long* messages, uint64_t* bytes, long* copy_events,
+                                      long max) {
+  const long n = (long)h->ledger.size();
+  for (long i = 0; i < std::min(n, max); ++i) {
+    const LedgerRow& e = h->ledger[i];
+    if (step) step[i] = e.step;
+    if (transport) transport[i] = e.transport;
+    if (messages) messages[i] = e.messages;
+    if (bytes) bytes[i] = e.bytes;
+    if (copy_events) copy_events[i] = e.copy_events;
+  }
+  return n;
+}
+
+// write_snapshot (snapshot.cpp:58-85) of make_snapshot (ppmlr_main.cpp:20-31):
+// "PPLR", u32 version 1, u32 dims[3], u32 ghost, f64 time, u64 step, the
+// global edge arrays, the tag "rvvvbbbp", then per field the global
+// interior array, x fastest.  Every block's capture is drained plane-chunk
+// by plane-chunk into one pinned global chunk and appended to the file.
+int ppmlr_gpu_harness_snapshot_begin(ppmlr_gpu_harness* h, const char* path) {
+  if (int rc = ppmlr_gpu_harness_snapshot_wait(h)) return rc;
+  for (auto* b : h->blocks)
+    if (int rc = ppmlr_gpu_block_snapshot_capture(b)) return rc;
+  struct Header {
+    uint32_t dims[3], ghost;
+    double time;
+    uint64_t step;
+  } hd{{(uint32_t)h->ax[0].n(), (uint32_t)h->ax[1].n(), (uint32_t)h->ax[2].n()},
+       (uint32_t)h->o.ghost, h->time, (uint64_t)h->step};
+  const std::string file = path;
+  h->snap_rc = 0;
+  h->snap_err.clear();
+  h->snap_writer = std::thread([h, hd, file] {
+    auto fail = [&](int rc, const std::string& m) {
+      h->snap_rc = rc;
+      h->snap_err = m;
+    };
+    cudaSetDevice(h->o.device);
+    FILE* out = std::fopen(file.c_str(), "wb");
+    if (!out) return fail(PPMLR_INVALID_SPEC, "snapshot: cannot open for writing: " + file);
+    const uint32_t version = 1;
+    bool ok = std::fwrite("PPLR", 1, 4, out) == 4 && std::fwrite(&version, 4, 1, out) == 1 &&
+              std::fwrite(hd.dims, 4, 3, out) == 3 && std::fwrite(&hd.ghost, 4, 1, out) == 1 &&
+              std::fwrite(&hd.time, 8, 1, out) == 1 && std::fwrite(&hd.step, 8, 1, out) == 1;
+    for (int a = 0; a < 3 && ok; ++a)
+      ok = std::fwrite(h->ax[a].edges.data(), 8, h->ax[a].edges.size(), out) ==
+           h->ax[a].edges.size();
+    ok = ok && std::fwrite("rvvvbbbp", 1, 8, out) == 8;
+    const size_t nx = hd.dims[0], ny = hd.dims[1], nz = hd.dims[2];
+    const size_t plane = nx * ny;
+    const size_t kchunk = std::max<size_t>(1, std::min<size_t>(nz, (64u << 20) / (plane * 8)));
+    double* buf = nullptr;
+    if (ok && cudaMallocHost(&buf, plane * kchunk * sizeof(double)) != cudaSuccess) {
+      std::fclose(out);
+      return fail(PPMLR_RUNTIME, "snapshot: pinned staging allocation failed");
+    }
+    for (int f = 0; f < 8 && ok; ++f)
+      for (size_t k0 = 0; k0 < nz && ok; k0 += kchunk) {
+        const size_t nk = std::min(kchunk, nz - k0);
+        for (size_t r = 0; r < h->blocks.size(); ++r) {
+          const BlockPlan& p = h->plan[r];
+          const long lo = std::max<long>(p.lo[2], (long)k0);
+          const long hi = std::min<long>(p.lo[2] + p.n[2], (long)(k0 + nk));
+          if (lo >= hi) continue;
+          double* dst = buf + (size_t)(lo - (long)k0) * plane + (size_t)p.lo[1] * nx + p.lo[0];
+          if (int rc = ppmlr_gpu_block_snapshot_read(h->blocks[r], f, (int)(lo - p.lo[2]),
+                                                     (int)(hi - lo), dst, (int64_t)nx,
+                                                     (int64_t)plane)) {
+            cudaFreeHost(buf);
+            std::fclose(out);
+            return fail(rc, ppmlr_gpu_last_error());
+          }
+        }
+        ok = std::fwrite(buf, 8, plane * nk, out) == plane * nk;
+      }
+    if (buf) cudaFreeHost(buf);
+    if (std::fclose(out) != 0) ok = false;
+    if (!ok) fail(PPMLR_INVALID_SPEC, "snapshot: write failed: " + file);
+  });
+  return 0;
+}
+
+int ppmlr_gpu_harness_snapshot_wait(ppmlr_gpu_harness* h) {
+  if (h->snap_writer.joinable()) h->snap_writer.join();
+  const int rc = h->snap_rc;
+  if (rc) set_error(h->snap_err);
+  h->snap_rc = 0;
+  return rc;
+}
+
+int ppmlr_gpu_harness_snapshot(ppmlr_gpu_harness* h, const char* path) {
+  if (int rc = ppmlr_gpu_harness_snapshot_begin(h, path)) return rc;
+  return ppmlr_gpu_harness_snapshot_wait(h);
 }
 
 int64_t ppmlr_gpu_harness_frozen(ppmlr_gpu_harness* h, int rank, int64_t* idx, double* states) {
