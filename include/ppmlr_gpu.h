@@ -215,6 +215,11 @@ int ppmlr_gpu_block_timing(ppmlr_gpu_block* b, int enable, double* sweep_ms,
 int ppmlr_gpu_sweep_strips(double* states, const double* bd, const double* dx, int n,
                            int ghost, int nstrips, int dir, double dt, double gamma,
                            double mu0, double pressure_floor, int precision, int device);
+/* strip_max_dt (ppm1d.cpp:307-315): min over the strips' interior cells of
+ * dx / (|v_dir| + c_f,dir), bit-identical to the reference (IEEE ops). */
+int ppmlr_gpu_strip_max_dt(const double* states, const double* bd, const double* dx, int n,
+                           int ghost, int nstrips, int dir, double gamma, double mu0,
+                           int device, double* dt_out);
 
 /* ------------------------------------------------------------------------
  * Harness (harness.hpp:48-87): all blocks of a layout in one process (each

@@ -259,6 +259,8 @@ def ref():
         lib.ref_harness_ledger_entries.argtypes = [vp] + [C.c_void_p] * 5 + [C.c_long]
         lib.ref_harness_ledger_entries.restype = C.c_long
         lib.ref_harness_write_snapshot.argtypes = [vp, C.c_char_p, C.c_char_p, C.c_int]
+        lib.ref_run_suite.argtypes = [C.c_char_p, _dp, C.POINTER(C.c_int), C.c_int,
+                                      C.c_char_p, C.c_int]
         lib.ref_bench.argtypes = [C.POINTER(RefAxisSpec), C.POINTER(RefOptions), C.c_int, _dp,
                                   C.c_int, C.c_int, _dp, _dp, C.c_char_p, C.c_int]
         _ref = lib
@@ -432,6 +434,16 @@ class RefHarness:
     def write_snapshot(self, path):
         err = C.create_string_buffer(512)
         self._chk(ref().ref_harness_write_snapshot(self.h, os.fsencode(path), err, 512), err)
+
+
+def ref_run_suite(name):
+    """The reference's verify suite `name`: [(metric, passed), ...]."""
+    m, p = np.zeros(8), (C.c_int * 8)()
+    err = C.create_string_buffer(512)
+    n = ref().ref_run_suite(name.encode(), _ptr(m), p, 8, err, 512)
+    if n < 0:
+        raise OracleError(-n, err.value.decode())
+    return [(float(m[i]), bool(p[i])) for i in range(n)]
 
 
 def ref_bench(specs, ic_kind, ic_params, threads, steps, **kw):

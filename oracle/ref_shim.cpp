@@ -19,6 +19,7 @@
 #include "ppmlr/snapshot.hpp"
 #include "ppmlr/ppm1d.hpp"
 #include "ppmlr/stepper.hpp"
+#include "ppmlr/verify.hpp"
 
 using namespace ppmlr;
 
@@ -380,6 +381,23 @@ long ref_harness_ledger_entries(void* h, long* step, int* transport, long* messa
     copy_events[i] = e[i].copy_events;
   }
   return n;
+}
+
+// run_suite (verify.cpp:234-243): metrics and pass flags of one suite.
+int ref_run_suite(const char* name, double* metrics, int* pass, int max, char* err,
+                  int errlen) {
+  int n = 0;
+  const int rc = guarded(err, errlen, [&] {
+    const auto res = run_suite(name);
+    for (const auto& r : res) {
+      if (n < max) {
+        metrics[n] = r.metric;
+        pass[n] = r.pass ? 1 : 0;
+      }
+      ++n;
+    }
+  });
+  return rc ? -rc : n;
 }
 
 // `ppmlr run`'s snapshot of the current state: make_snapshot

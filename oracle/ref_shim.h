@@ -86,6 +86,9 @@ long ref_harness_ledger_messages(void* h);
 long ref_harness_ledger_copy_events(void* h);
 long ref_harness_ledger_entries(void* h, long* step, int* transport, long* messages,
                                 uint64_t* bytes, long* copy_events, long max);
+/* run_suite (verify.cpp:234-243): count of checks (or -rc on error). */
+int ref_run_suite(const char* name, double* metrics, int* pass, int max, char* err,
+                  int errlen);
 int ref_harness_write_snapshot(void* h, const char* path, char* err, int errlen);
 
 /* CPU baseline: `threads` independent harnesses (one per thread) built from

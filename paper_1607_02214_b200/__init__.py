@@ -10,6 +10,6 @@ from .api import (FAST, IC_BLAST, IC_BRIOWU, IC_GAUSSIAN, IC_ORSZAG_TANG, IC_PAR
                   AxisSpec, Block, BlockInfo, Error, Harness, HarnessOptions, InvalidSpec,
                   OutOfRange, RuntimeFailure, SolarWindParams, StepRejected, UnphysicalState,
                   build_axis, device_count, exchanged_bytes, host_block_state, layout,
-                  sweep_strips, tde_units, version)
+                  strip_max_dt, sweep_strips, tde_units, version)
 
 __all__ = [n for n in dir() if not n.startswith("_")]

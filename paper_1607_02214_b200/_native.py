@@ -162,6 +162,8 @@ _sig("ppmlr_gpu_harness_block", _vp, _vp, C.c_int)
 _sig("ppmlr_gpu_harness_ledger", None, _vp, C.POINTER(C.c_uint64), C.POINTER(C.c_long),
      C.POINTER(C.c_long))
 _sig("ppmlr_gpu_harness_frozen", C.c_int64, _vp, C.c_int, _i64p, _dp)
+_sig("ppmlr_gpu_strip_max_dt", C.c_int, _dp, _dp, _dp, C.c_int, C.c_int, C.c_int, C.c_int,
+     C.c_double, C.c_double, C.c_int, _dp)
 _sig("ppmlr_gpu_harness_ledger_entries", C.c_long, _vp, C.POINTER(C.c_long),
      C.POINTER(C.c_int), C.POINTER(C.c_long), C.POINTER(C.c_uint64), C.POINTER(C.c_long),
      C.c_long)

@@ -423,6 +423,24 @@ def sweep_strips(states, bd, dx, n, ghost, dt, direction, gamma=5.0 / 3.0, mu0=1
     return states
 
 
+def strip_max_dt(states, bd, dx, n, ghost, direction, gamma=5.0 / 3.0, mu0=1.0, device=0):
+    """strip_max_dt (ppm1d.cpp:307-315) on the device: the min over the
+    strips' interior cells of dx / (|v_dir| + c_f,dir), bit-identical."""
+    states = np.ascontiguousarray(states, dtype=np.float64)
+    if states.ndim == 2:
+        states = states[None]
+    ns = states.shape[0]
+    bdp = None
+    if bd is not None:
+        bd = np.ascontiguousarray(bd, dtype=np.float64).reshape(ns, n + 2 * ghost, 3)
+        bdp = ptr(bd)
+    dx = np.ascontiguousarray(dx, dtype=np.float64)
+    out = C.c_double()
+    check(N.lib.ppmlr_gpu_strip_max_dt(ptr(states), bdp, ptr(dx), n, ghost, ns, direction,
+                                       gamma, mu0, device, C.byref(out)))
+    return out.value
+
+
 def version():
     return N.lib.ppmlr_gpu_version().decode()
 

@@ -1382,6 +1382,88 @@ int ppmlr_gpu_block_timing(ppmlr_gpu_block* b, int enable, double* sweep_ms, dou
   return 0;
 }
 
+}  // extern "C"
+
+namespace {
+// strip_max_dt (ppm1d.cpp:307-315) over a batch of strips: min over every
+// interior cell of dx / (|v_dir| + c_f,dir), physics::fast_speed in xyz
+// order with the plain IEEE operations (ExactOps); NaN candidates drop out
+// like std::min's, and the min of the per-strip minima is the global one.
+template <int DIR>
+__global__ void strip_dt_kernel(const double* __restrict__ st, const double* __restrict__ bd,
+                                const double* __restrict__ dx, int n, int g, int ns, Consts cc,
+                                unsigned long long* out) {
+  const KC k = make_kc(cc);
+  const long long total = (long long)ns * n;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long strip = t / n;
+    const int i = (int)(t - strip * n);
+    const long long idx = strip * (n + 2 * g) + g + i;
+    const double* s = st + 8 * idx;
+    const double b0 = bd ? bd[3 * idx] : 0.0, b1 = bd ? bd[3 * idx + 1] : 0.0,
+                 b2 = bd ? bd[3 * idx + 2] : 0.0;
+    ExactOps o;
+    const double cf = fast_speed3<DIR>(s, b0, b1, b2, k, o);
+    const double speed = fabs(s[1 + DIR]) + cf;
+    const double cand = dx[g + i] / speed;
+    if (cand < INFINITY) atomicMin(out, (unsigned long long)__double_as_longlong(cand));
+  }
+}
+}  // namespace
+
+extern "C" {
+
+int ppmlr_gpu_strip_max_dt(const double* states, const double* bd, const double* dx, int n,
+                           int ghost, int nstrips, int dir, double gamma, double mu0,
+                           int device, double* dt_out) {
+  if (n < 1 || ghost < 0 || nstrips < 1 || dir < 0 || dir > 2) {
+    set_error("strip_max_dt: bad strip description");
+    return PPMLR_INVALID_SPEC;
+  }
+  CK(cudaSetDevice(device));
+  const size_t nn = (size_t)n + 2 * ghost, cells = nn * nstrips;
+  double *d_st = nullptr, *d_bd = nullptr, *d_dx = nullptr;
+  unsigned long long* d_out = nullptr;
+  auto release = [&] {
+    cudaFree(d_st);
+    cudaFree(d_bd);
+    cudaFree(d_dx);
+    cudaFree(d_out);
+  };
+  cudaError_t e = cudaMalloc(&d_st, cells * 64);
+  if (e == cudaSuccess && bd) e = cudaMalloc(&d_bd, cells * 24);
+  if (e == cudaSuccess) e = cudaMalloc(&d_dx, nn * 8);
+  if (e == cudaSuccess) e = cudaMalloc(&d_out, 8);
+  if (e == cudaSuccess) e = cudaMemcpy(d_st, states, cells * 64, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && bd) e = cudaMemcpy(d_bd, bd, cells * 24, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(d_dx, dx, nn * 8, cudaMemcpyHostToDevice);
+  const unsigned long long inf = kInfBits;
+  if (e == cudaSuccess) e = cudaMemcpy(d_out, &inf, 8, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    release();
+    return cuda_fail(e, "strip_max_dt setup");
+  }
+  Consts c{};
+  c.gamma = gamma;
+  c.mu0 = mu0;
+  c.gm1 = gamma - 1.0;
+  c.two_mu0 = 2.0 * mu0;
+  const long long work = (long long)n * nstrips;
+  switch (dir) {
+    case 0: strip_dt_kernel<0><<<grid_for(work), 256>>>(d_st, d_bd, d_dx, n, ghost, nstrips, c, d_out); break;
+    case 1: strip_dt_kernel<1><<<grid_for(work), 256>>>(d_st, d_bd, d_dx, n, ghost, nstrips, c, d_out); break;
+    default: strip_dt_kernel<2><<<grid_for(work), 256>>>(d_st, d_bd, d_dx, n, ghost, nstrips, c, d_out); break;
+  }
+  unsigned long long bits = inf;
+  e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaMemcpy(&bits, d_out, 8, cudaMemcpyDeviceToHost);
+  release();
+  if (e != cudaSuccess) return cuda_fail(e, "strip_max_dt");
+  std::memcpy(dt_out, &bits, 8);
+  return 0;
+}
+
 int ppmlr_gpu_sweep_strips(double* states, const double* bd, const double* dx, int n,
                            int ghost, int nstrips, int dir, double dt, double gamma,
                            double mu0, double pressure_floor, int precision, int device) {
