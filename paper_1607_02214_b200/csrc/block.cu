@@ -129,13 +129,15 @@ __global__ void interior_planes_kernel(double* __restrict__ out, Planes src, Lay
   }
 }
 
-__global__ void soa_to_interior_kernel(double* __restrict__ out, Planes src, Lay L) {
-  const long long total = (long long)L.n0 * L.n1 * L.n2;
+// Interior k-planes [k0, k0 + nk) as AoS, x fastest (gather_interior order).
+__global__ void soa_to_interior_kernel(double* __restrict__ out, Planes src, Lay L, int k0,
+                                       int nk) {
+  const long long total = (long long)L.n0 * L.n1 * nk;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
        t += (long long)gridDim.x * blockDim.x) {
     const int i = (int)(t % L.n0);
     const int j = (int)((t / L.n0) % L.n1);
-    const int k = (int)(t / ((long long)L.n0 * L.n1));
+    const int k = k0 + (int)(t / ((long long)L.n0 * L.n1));
     const long long d = L.idx(i, j, k);
     for (int f = 0; f < 8; ++f) out[t * 8 + f] = src.f[f][d];
   }
@@ -909,7 +911,8 @@ int block_set_frozen(ppmlr_gpu_block* b, const int64_t* frozen_idx, const double
 // k-planes [kr0, kr0+nk) (bd only when the block carries the dipole) into
 // pinned staging; each chunk is copied and converted while the next is
 // filled.  No full-size host copy of the state is needed.
-int block_upload_streamed(ppmlr_gpu_block* b, const ChunkFill& fill, bool with_bd) {
+int block_upload_streamed(ppmlr_gpu_block* b, const ChunkFill& fill, bool with_bd,
+                          const double* src_fields, const double* src_bd) {
   CK(cudaSetDevice(b->device));
   CK(cudaStreamSynchronize(b->stream));
   const int gr = b->g_ref;
@@ -920,10 +923,13 @@ int block_upload_streamed(ppmlr_gpu_block* b, const ChunkFill& fill, bool with_b
   const int kchunk = (int)std::max<size_t>(1, std::min<size_t>(S2r, (64ull << 20) / (plane * 8 * nper)));
   const size_t chunk_doubles = plane * kchunk * nper;
   if (int rc = ensure_scratch(b, 2 * chunk_doubles * sizeof(double))) return rc;
+  // src_fields given: copy straight from the caller's buffers (pinned
+  // memory DMAs at full PCIe rate); otherwise fill pinned staging chunks
+  const bool direct = src_fields != nullptr;
   double* host[2] = {nullptr, nullptr};
   cudaEvent_t done[2] = {nullptr, nullptr};
   for (int q = 0; q < 2; ++q) {
-    CK(cudaMallocHost(&host[q], chunk_doubles * sizeof(double)));
+    if (!direct) CK(cudaMallocHost(&host[q], chunk_doubles * sizeof(double)));
     CK(cudaEventCreateWithFlags(&done[q], cudaEventDisableTiming));
   }
   const Lay L = lay_of(b);
@@ -932,12 +938,24 @@ int block_upload_streamed(ppmlr_gpu_block* b, const ChunkFill& fill, bool with_b
   for (int kr0 = 0; kr0 < S2r && !rc; kr0 += kchunk, q ^= 1) {
     const int nk = std::min(kchunk, S2r - kr0);
     CK(cudaEventSynchronize(done[q]));  // staging buffer q free again
-    double* hf = host[q];
-    double* hb = with_bd ? host[q] + plane * nk * 8 : nullptr;
-    fill(kr0, nk, hf, hb);
     double* dscr = b->d_scratch + q * chunk_doubles;
-    CK(cudaMemcpyAsync(dscr, hf, plane * nk * nper * sizeof(double), cudaMemcpyHostToDevice,
-                       b->stream));
+    const double* hb = nullptr;
+    if (direct) {
+      CK(cudaMemcpyAsync(dscr, src_fields + plane * kr0 * 8, plane * nk * 8 * sizeof(double),
+                         cudaMemcpyHostToDevice, b->stream));
+      if (with_bd) {
+        CK(cudaMemcpyAsync(dscr + plane * nk * 8, src_bd + plane * kr0 * 3,
+                           plane * nk * 3 * sizeof(double), cudaMemcpyHostToDevice, b->stream));
+        hb = src_bd;
+      }
+    } else {
+      double* hf = host[q];
+      double* hbw = with_bd ? host[q] + plane * nk * 8 : nullptr;
+      fill(kr0, nk, hf, hbw);
+      hb = hbw;
+      CK(cudaMemcpyAsync(dscr, hf, plane * nk * nper * sizeof(double), cudaMemcpyHostToDevice,
+                         b->stream));
+    }
     for (int k = 0; k < 2; ++k)
       aos_to_soa_kernel<<<grid_for(plane * nk), 256, 0, b->stream>>>(
           dscr, 8, planes(b->buf[k], b->ncell), L, gr, S0r, S1r, kr0, nk,
@@ -949,7 +967,7 @@ int block_upload_streamed(ppmlr_gpu_block* b, const ChunkFill& fill, bool with_b
   }
   cudaStreamSynchronize(b->stream);
   for (int k = 0; k < 2; ++k) {
-    cudaFreeHost(host[k]);
+    if (host[k]) cudaFreeHost(host[k]);
     cudaEventDestroy(done[k]);
   }
   if (rc) return rc;
@@ -985,26 +1003,29 @@ extern "C" {
 int ppmlr_gpu_block_upload(ppmlr_gpu_block* b, const double* fields, const double* bd,
                            const int64_t* frozen_idx, const double* frozen_states,
                            int64_t n_frozen) {
-  const int gr = b->g_ref;
-  const size_t plane = (size_t)(b->n[0] + 2 * gr) * (b->n[1] + 2 * gr);
   const bool with_bd = b->with_dipole && bd != nullptr;
   if (int rc = block_set_frozen(b, frozen_idx, frozen_states, n_frozen)) return rc;
-  return block_upload_streamed(b, [&](int kr0, int nk, double* hf, double* hb) {
-    std::memcpy(hf, fields + plane * kr0 * 8, plane * nk * 8 * sizeof(double));
-    if (hb) std::memcpy(hb, bd + plane * kr0 * 3, plane * nk * 3 * sizeof(double));
-  }, with_bd);
+  return block_upload_streamed(b, ChunkFill(), with_bd, fields, bd);
 }
 
 static int download_impl(ppmlr_gpu_block* b, double* fields, bool interior_only) {
   CK(cudaSetDevice(b->device));
   const Lay L = lay_of(b);
-  if (interior_only) {
-    const size_t cells = (size_t)b->n[0] * b->n[1] * b->n[2];
-    if (int rc = ensure_scratch(b, cells * 64)) return rc;
-    soa_to_interior_kernel<<<grid_for(cells), 256, 0, b->stream>>>(
-        b->d_scratch, planes(cur_buf(b), b->ncell), L);
-    CK(cudaGetLastError());
-    CK(cudaMemcpyAsync(fields, b->d_scratch, cells * 64, cudaMemcpyDeviceToHost, b->stream));
+  if (interior_only) {  // k-chunks through two 64 MB scratch halves
+    const size_t plane = (size_t)b->n[0] * b->n[1];
+    const int kchunk = (int)std::max<size_t>(1, std::min<size_t>(b->n[2], (64ull << 20) / (plane * 64)));
+    const size_t half = plane * kchunk * 8;
+    if (int rc = ensure_scratch(b, 2 * half * sizeof(double))) return rc;
+    int q = 0;
+    for (int k0 = 0; k0 < b->n[2]; k0 += kchunk, q ^= 1) {
+      const int nk = std::min(kchunk, b->n[2] - k0);
+      double* dscr = b->d_scratch + q * half;
+      soa_to_interior_kernel<<<grid_for(plane * nk), 256, 0, b->stream>>>(
+          dscr, planes(cur_buf(b), b->ncell), L, k0, nk);
+      CK(cudaGetLastError());
+      CK(cudaMemcpyAsync(fields + plane * k0 * 8, dscr, plane * nk * 64, cudaMemcpyDeviceToHost,
+                         b->stream));
+    }
     CK(cudaStreamSynchronize(b->stream));
     return 0;
   }

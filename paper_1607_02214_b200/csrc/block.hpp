@@ -131,6 +131,9 @@ int block_set_dt(ppmlr_gpu_block* b, double dt);  // dt < 0: keep the device slo
 using ChunkFill = std::function<void(int kr0, int nk, double* fields, double* bd)>;
 int block_set_frozen(ppmlr_gpu_block* b, const int64_t* frozen_idx, const double* frozen_states,
                      int64_t n_frozen);
-int block_upload_streamed(ppmlr_gpu_block* b, const ChunkFill& fill, bool with_bd);
+// With src_fields (and src_bd) given, chunks are copied straight from those
+// caller buffers and `fill` is unused.
+int block_upload_streamed(ppmlr_gpu_block* b, const ChunkFill& fill, bool with_bd,
+                          const double* src_fields = nullptr, const double* src_bd = nullptr);
 int block_finish_upload(ppmlr_gpu_block* b);
 }  // namespace ppmlr_b200
