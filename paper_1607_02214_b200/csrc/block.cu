@@ -2,6 +2,8 @@
 // reduction, dipole source terms, frozen core, halo pack/unpack and the
 // per-step CUDA graph.  Compiled with --fmad=false so every arithmetic
 // kernel here is bit-identical to the reference (proj/src/stepper.cpp).
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -464,6 +466,7 @@ void choose_sweep_tiles(ppmlr_gpu_block* b) {
     } else {
       const int nseg = (n + Lmax - 1) / Lmax;
       L = (n + nseg - 1) / nseg;
+      L += L & 1;  // even: the x tile box row (TL doubles) must be a multiple of 16 B
     }
     b->sweep_L[a] = L;
     const int T = 4 * (L + 8);
@@ -516,16 +519,16 @@ int launch_sweep(ppmlr_gpu_block* b, int axis, int phase) {
   A.c = b->c;
   A.redo_count = b->d_redo;
   A.redo_list = b->d_redo + 1;
-  const int T = 4 * (A.L + 8);
+  const int T = slot_stride(4 * (A.L + 8));
   const int slots = 25 + (b->with_dipole ? 3 : 0);
   const size_t smem = sizeof(double) * (size_t)T * slots;
   // The sweep writes only the interior of the output buffer; its ghost
   // shells stay stale until the next fill (every reader fills first).
   cudaError_t e = b->precision == PPMLR_FAST
-                      ? launch_sweep_fast(axis, b->with_dipole, A, b->sweep_threads[axis], smem,
-                                          b->stream)
-                      : launch_sweep_strict(axis, b->with_dipole, A, b->sweep_threads[axis],
-                                            smem, b->stream);
+                      ? launch_sweep_fast(axis, b->with_dipole, A, b->maps[3 * b->cur + axis],
+                                          b->sweep_threads[axis], smem, b->stream)
+                      : launch_sweep_strict(axis, b->with_dipole, A, b->maps[3 * b->cur + axis],
+                                            b->sweep_threads[axis], smem, b->stream);
   if (e != cudaSuccess) return cuda_fail(e, "sweep kernel launch");
   b->kernel_launches += 2;  // fast pass + exact re-run of flagged tiles
   b->cur ^= 1;
@@ -643,6 +646,53 @@ int block_set_dt(ppmlr_gpu_block* b, double dt) {
 }  // namespace ppmlr_b200
 
 // ---------------------------------------------------------------- C-ABI
+
+namespace {
+// TMA descriptors of the sweep inputs for both ping-pong buffers and every
+// axis: each field / dipole plane as a 3-D tensor {S0, S1, S2} (x pitch P0)
+// with the axis' tile box (sweep.cuh SweepMaps).  cuTensorMapEncodeTiled is
+// reached through the runtime's driver entry point (no -lcuda).
+int build_sweep_maps(ppmlr_gpu_block* b) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn) {
+      set_error("cuTensorMapEncodeTiled unavailable");
+      return PPMLR_RUNTIME;
+    }
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  b->maps = new SweepMaps[6];
+  std::memset(static_cast<void*>(b->maps), 0, sizeof(SweepMaps) * 6);
+  const cuuint64_t dims[3] = {(cuuint64_t)b->S[0], (cuuint64_t)b->S[1], (cuuint64_t)b->S[2]};
+  const cuuint64_t strides[2] = {(cuuint64_t)b->sy * 8, (cuuint64_t)b->sz * 8};
+  const cuuint32_t elem[3] = {1, 1, 1};
+  // tile box per axis: TL = L + 8 strip positions x 4 pencils
+  const cuuint32_t t0 = b->sweep_L[0] + 8, t1 = b->sweep_L[1] + 8, t2 = b->sweep_L[2] + 8;
+  const cuuint32_t box[3][3] = {{t0, 4, 1}, {4, t1, 1}, {4, 1, t2}};
+  for (int k = 0; k < 2; ++k)
+    for (int a = 0; a < 3; ++a) {
+      SweepMaps& m = b->maps[3 * k + a];
+      for (int f = 0; f < 11; ++f) {
+        if (f >= 8 && !b->bd) break;
+        double* base = f < 8 ? b->buf[k] + f * b->ncell : b->bd + (f - 8) * b->ncell;
+        CUtensorMap* t = f < 8 ? &m.f[f] : &m.bd[f - 8];
+        const CUresult r = encode(t, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides,
+                                  box[a], elem, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) {
+          set_error("cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+          return PPMLR_RUNTIME;
+        }
+      }
+    }
+  return 0;
+}
+}  // namespace
 
 extern "C" {
 
@@ -782,6 +832,7 @@ int ppmlr_gpu_block_create(const ppmlr_gpu_block_desc* d, ppmlr_gpu_block** out)
   if ((e = cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking)) != cudaSuccess)
     return fail(cuda_fail(e, "cudaStreamCreate"));
   choose_sweep_tiles(b);
+  if (int rc = build_sweep_maps(b)) return fail(rc);
   {
     long long tiles = 1;
     for (int a = 0; a < 3; ++a) {
@@ -818,6 +869,7 @@ void ppmlr_gpu_block_destroy(ppmlr_gpu_block* b) {
     cudaFree(b->ax[a].den);
     cudaFree(b->ax[a].rden);
   }
+  delete[] b->maps;
   if (b->snap_stream) cudaStreamSynchronize(b->snap_stream);
   cudaFree(b->d_snap);
   if (b->snap_stream) cudaStreamDestroy(b->snap_stream);

@@ -44,6 +44,10 @@ struct StepGraph {
 
 }  // namespace ppmlr_b200
 
+namespace ppmlr_b200 {
+struct SweepMaps;
+}
+
 struct ppmlr_gpu_block {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -99,6 +103,8 @@ struct ppmlr_gpu_block {
   double* d_snap = nullptr;
   cudaStream_t snap_stream = nullptr;
   cudaEvent_t snap_ready = nullptr;
+  // TMA descriptors of the sweep inputs: [source buffer][axis] (block.cu)
+  ppmlr_b200::SweepMaps* maps = nullptr;
 };
 
 namespace ppmlr_b200 {
@@ -106,13 +112,14 @@ void set_error(const std::string& msg);
 int cuda_fail(cudaError_t e, const char* where);
 // Launchers implemented in sweep_*.cu
 struct SweepArgs;
-cudaError_t launch_sweep_strict(int axis, bool dipole, const SweepArgs& a, int threads,
-                                size_t smem, cudaStream_t st);
+struct SweepMaps;
+cudaError_t launch_sweep_strict(int axis, bool dipole, const SweepArgs& a, const SweepMaps& m,
+                                int threads, size_t smem, cudaStream_t st);
 struct SrcArgs;
 cudaError_t launch_sources_strict(const SrcArgs& a, bool dipole, cudaStream_t st);
 cudaError_t launch_sources_fast(const SrcArgs& a, bool dipole, cudaStream_t st);
-cudaError_t launch_sweep_fast(int axis, bool dipole, const SweepArgs& a, int threads,
-                              size_t smem, cudaStream_t st);
+cudaError_t launch_sweep_fast(int axis, bool dipole, const SweepArgs& a, const SweepMaps& m,
+                              int threads, size_t smem, cudaStream_t st);
 }  // namespace ppmlr_b200
 
 namespace ppmlr_b200 {

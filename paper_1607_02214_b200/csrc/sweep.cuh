@@ -30,6 +30,8 @@
 // main instance runs branch-free fast paths and flags tiles whose guards
 // failed; the EXACT instance re-runs those tiles with plain `/` and `sqrt`.
 #pragma once
+#include <cuda.h>  // CUtensorMap (the maps are encoded on the host, block.cu)
+
 #include "ppmlr_dev.cuh"
 
 namespace ppmlr_b200 {
@@ -40,9 +42,23 @@ constexpr int kSweepTL = 72;
 #ifndef PPMLR_SWEEP_MINB
 #define PPMLR_SWEEP_MINB 3  // resident CTAs per SM the register budget targets
 #endif
+#ifndef PPMLR_SWEEP_TMA
+#define PPMLR_SWEEP_TMA 1  // TMA tile loads for the compile-time tile
+#endif
 #ifndef PPMLR_SWEEP_CSLOPE
 #define PPMLR_SWEEP_CSLOPE 1  // conserved slopes once per cell (P7b) vs per moving edge
 #endif
+
+// TMA descriptors of the sweep's input: the 8 field planes of the source
+// buffer and the 3 dipole planes, each a 3-D (x, y, z) tensor over the padded
+// ghost-inclusive block with the tile box of this axis ({72,4,1} for x,
+// {4,72,1} for y, {4,1,72} for z; TL = L + 8 of the block's axis in
+// place of 72 for the runtime tile).  The box lands in shared memory in
+// exactly the tile's cell order (ci), one field per slot.
+struct SweepMaps {
+  CUtensorMap f[8];
+  CUtensorMap bd[3];
+};
 
 struct SweepArgs {
   const double* src[8];  // field planes of the input buffer (padded block layout)
@@ -119,13 +135,67 @@ __device__ __forceinline__ void zone_parabola_dm(const W& q, const D& dm, const 
   limit_parabola(al, ar, q(0), six, k, o);
 }
 
-template <int AXIS, bool DIPOLE, int NP, int TLC, class Ops>
+// Shared slots start on 128-byte boundaries (the TMA destination rule).
+__host__ __device__ constexpr int slot_stride(int cells) { return (cells + 15) & ~15; }
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+
+// One elected thread: expect the tile's bytes on `mbar` and issue the TMA
+// loads of the 8 fields (+3 dipole planes) into SA / BD.
+template <int AXIS, bool DIPOLE, int NP, int TLC>
+__device__ __forceinline__ void tma_load_tile(const SweepArgs& A, const SweepMaps& M, int seg,
+                                              int grp, int oc, double* smem,
+                                              unsigned long long* mbar) {
+  const int NT = NP * (TLC > 0 ? TLC : A.L + 8);
+  const int T = slot_stride(NT);
+  const unsigned kBox = NT * sizeof(double);
+  const int a0 = seg * A.L, g = grp * NP + 4, o = oc + 4;
+  const int cx = AXIS == 0 ? a0 : g;
+  const int cy = AXIS == 0 ? g : (AXIS == 1 ? a0 : o);
+  const int cz = AXIS == 2 ? a0 : o;
+  const unsigned bar = smem_u32(mbar);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+               "r"(kBox * (DIPOLE ? 11u : 8u))
+               : "memory");
+  double* SA = smem + 17 * T;
+  double* BD = smem + 25 * T;
+#pragma unroll
+  for (int f = 0; f < 8 + (DIPOLE ? 3 : 0); ++f) {
+    const CUtensorMap* m = f < 8 ? &M.f[f] : &M.bd[f - 8];
+    double* dst = f < 8 ? SA + f * T : BD + (f - 8) * T;
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<unsigned long long>(m)), "r"(cx), "r"(cy), "r"(cz), "r"(bar)
+        : "memory");
+  }
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned long long* mbar, unsigned parity) {
+  const unsigned bar = smem_u32(mbar);
+  unsigned done = 0;
+  while (!done)
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; "
+        "selp.b32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+}
+
+// TMA: the tile's inputs arrive in SA / BD through tma_load_tile (issued by
+// the caller, completing on `mbar`) instead of per-thread global loads.
+template <int AXIS, bool DIPOLE, int NP, int TLC, class Ops, bool TMA = false>
 __device__ __forceinline__ bool sweep_tile(const SweepArgs& A, const int seg, const int grp,
                                            const int oc, double* smem,
-                                           unsigned long long* s_err) {
+                                           unsigned long long* s_err,
+                                           unsigned long long* mbar = nullptr) {
   bool tbad = false;
   const int TL = TLC > 0 ? TLC : A.L + 8;
-  const int T = NP * TL;
+  const int NT = NP * TL;          // cells of the tile
+  const int T = slot_stride(NT);   // doubles per shared slot (128 B multiple)
   double* PRIM = smem;
   double* CONS = smem + 8 * T;
   double* CF = smem + 16 * T;
@@ -155,7 +225,7 @@ __device__ __forceinline__ bool sweep_tile(const SweepArgs& A, const int seg, co
     s = ci / NP;
     p = ci - s * NP;
   }
-  const bool live = ci < T && p < npv;
+  const bool live = ci < NT && p < npv;
   const int q = seg0 + s;
   auto pencil_index = [&]() -> unsigned long long {
     const int gcoord = g0 + p;
@@ -166,16 +236,17 @@ __device__ __forceinline__ bool sweep_tile(const SweepArgs& A, const int seg, co
   constexpr int a = AXIS, b = (AXIS + 1) % 3, d = (AXIS + 2) % 3;
 
   // ---- P0 ---------------------------------------------------------------
+  if (TMA) mbar_wait(mbar, 0);
   if (live && s < TLv) {
     const long long off = base + (long long)p * A.stride_g + (long long)s * A.stride_a;
     double qv[8];
 #pragma unroll
-    for (int f = 0; f < 8; ++f) qv[f] = __ldg(A.src[f] + off);
+    for (int f = 0; f < 8; ++f) qv[f] = TMA ? SA[f * T + ci] : __ldg(A.src[f] + off);
     double b0 = 0.0, b1 = 0.0, b2 = 0.0;
     if (DIPOLE) {
-      b0 = __ldg(A.bd[0] + off);
-      b1 = __ldg(A.bd[1] + off);
-      b2 = __ldg(A.bd[2] + off);
+      b0 = TMA ? BD[ci] : __ldg(A.bd[0] + off);
+      b1 = TMA ? BD[T + ci] : __ldg(A.bd[1] + off);
+      b2 = TMA ? BD[2 * T + ci] : __ldg(A.bd[2] + off);
       BD[0 * T + ci] = AXIS == 0 ? b0 : (AXIS == 1 ? b1 : b2);
       BD[1 * T + ci] = AXIS == 0 ? b1 : (AXIS == 1 ? b2 : b0);
       BD[2 * T + ci] = AXIS == 0 ? b2 : (AXIS == 1 ? b0 : b1);
@@ -478,9 +549,11 @@ using MainOps = FastOps;      // bit-exact replay of nvcc's fast paths
 // commits its error keys and results, otherwise it is queued for EXACT,
 // which re-runs the queued tiles with plain `/` and `sqrt`.
 template <int AXIS, bool DIPOLE, int NP, int TLC, bool EXACT>
-__global__ void __launch_bounds__(NP * kSweepTL, PPMLR_SWEEP_MINB) sweep_kernel(const SweepArgs A) {
-  extern __shared__ double smem[];
+__global__ void __launch_bounds__(NP * kSweepTL, PPMLR_SWEEP_MINB)
+    sweep_kernel(const SweepArgs A, const __grid_constant__ SweepMaps M) {
+  extern __shared__ __align__(128) double smem[];
   __shared__ unsigned long long s_err;
+  __shared__ __align__(8) unsigned long long s_mbar;
   if (EXACT) {
     const unsigned n = *A.redo_count;
     for (unsigned i = blockIdx.x; i < n; i += gridDim.x) {
@@ -494,11 +567,22 @@ __global__ void __launch_bounds__(NP * kSweepTL, PPMLR_SWEEP_MINB) sweep_kernel(
     }
     return;
   }
-  if (threadIdx.x == 0) s_err = kNoError;
+  // grid = (nseg, ngroups, no): the tile coordinates need no division.
+  // The tile's inputs stream in with TMA (boxes sized to the block's tile).
+  constexpr bool kTma = PPMLR_SWEEP_TMA;
+  if (threadIdx.x == 0) {
+    s_err = kNoError;
+    if (kTma) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&s_mbar)) : "memory");
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      tma_load_tile<AXIS, DIPOLE, NP, TLC>(A, M, blockIdx.x, blockIdx.y, blockIdx.z, smem,
+                                           &s_mbar);
+    }
+  }
   __syncthreads();
-  // grid = (nseg, ngroups, no): the tile coordinates need no division
-  const bool bad = sweep_tile<AXIS, DIPOLE, NP, TLC, MainOps>(A, blockIdx.x, blockIdx.y,
-                                                              blockIdx.z, smem, &s_err);
+  const bool bad = sweep_tile<AXIS, DIPOLE, NP, TLC, MainOps, kTma>(
+      A, blockIdx.x, blockIdx.y, blockIdx.z, smem, &s_err, &s_mbar);
   if (__syncthreads_or(bad)) {
     if (threadIdx.x == 0)
       A.redo_list[atomicAdd(A.redo_count, 1u)] =
