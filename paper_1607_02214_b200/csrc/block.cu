@@ -667,6 +667,8 @@ int build_sweep_maps(ppmlr_gpu_block* b) {
   }
   b->maps = new SweepMaps[6];
   std::memset(static_cast<void*>(b->maps), 0, sizeof(SweepMaps) * 6);
+  const cuuint32_t l0 = b->sweep_L[0], l1 = b->sweep_L[1], l2 = b->sweep_L[2];
+  const cuuint32_t obox[3][3] = {{l0, 4, 1}, {4, l1, 1}, {4, 1, l2}};
   const cuuint64_t dims[3] = {(cuuint64_t)b->S[0], (cuuint64_t)b->S[1], (cuuint64_t)b->S[2]};
   const cuuint64_t strides[2] = {(cuuint64_t)b->sy * 8, (cuuint64_t)b->sz * 8};
   const cuuint32_t elem[3] = {1, 1, 1};
@@ -683,6 +685,17 @@ int build_sweep_maps(ppmlr_gpu_block* b) {
         const CUresult r = encode(t, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides,
                                   box[a], elem, CU_TENSOR_MAP_INTERLEAVE_NONE,
                                   CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) {
+          set_error("cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+          return PPMLR_RUNTIME;
+        }
+      }
+      for (int f = 0; f < 8; ++f) {  // results go to the other buffer
+        const CUresult r = encode(&m.out[f], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3,
+                                  b->buf[k ^ 1] + f * b->ncell, dims, strides, obox[a], elem,
+                                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                  CU_TENSOR_MAP_L2_PROMOTION_NONE,
                                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) {
           set_error("cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");

@@ -45,6 +45,9 @@ constexpr int kSweepTL = 72;
 #ifndef PPMLR_SWEEP_TMA
 #define PPMLR_SWEEP_TMA 1  // TMA tile loads for the compile-time tile
 #endif
+#ifndef PPMLR_SWEEP_TMA_STORE
+#define PPMLR_SWEEP_TMA_STORE 1  // TMA stores of whole tiles' results
+#endif
 #ifndef PPMLR_SWEEP_CSLOPE
 #define PPMLR_SWEEP_CSLOPE 1  // conserved slopes once per cell (P7b) vs per moving edge
 #endif
@@ -58,6 +61,7 @@ constexpr int kSweepTL = 72;
 struct SweepMaps {
   CUtensorMap f[8];
   CUtensorMap bd[3];
+  CUtensorMap out[8];  // destination planes, box of the L interior zones
 };
 
 struct SweepArgs {
@@ -191,7 +195,8 @@ template <int AXIS, bool DIPOLE, int NP, int TLC, class Ops, bool TMA = false>
 __device__ __forceinline__ bool sweep_tile(const SweepArgs& A, const int seg, const int grp,
                                            const int oc, double* smem,
                                            unsigned long long* s_err,
-                                           unsigned long long* mbar = nullptr) {
+                                           unsigned long long* mbar = nullptr,
+                                           const SweepMaps* M = nullptr) {
   bool tbad = false;
   const int TL = TLC > 0 ? TLC : A.L + 8;
   const int NT = NP * TL;          // cells of the tile
@@ -206,10 +211,13 @@ __device__ __forceinline__ bool sweep_tile(const SweepArgs& A, const int seg, co
   const int nn = A.n + 8;
   const int seg0 = seg * A.L;
   const int TLv = min(TL, nn - seg0);
+  // TMA store of the results only for whole tiles (a partial box would
+  // write ghost or padding cells)
   const bool final_seg = seg == A.nseg - 1;
   const int zmax = final_seg ? TLv - 2 : TL - 3;
   const int g0 = grp * NP;
   const int npv = min(NP, A.ng - g0);
+  const bool tma_store = TMA && PPMLR_SWEEP_TMA_STORE && TLv == TL && npv == NP;
   const double dt = *A.dt;
   const Consts& c = A.c;
   const KC k = make_kc(c);
@@ -529,10 +537,35 @@ __device__ __forceinline__ bool sweep_tile(const SweepArgs& A, const int seg, co
                                (pencil_index() << 20) | (1ull << 19) |
                                    ((unsigned long long)(q - 4) << 2) |
                                    (bad == 1 ? kErrDensity : kErrPressure)));
+    } else if (tma_store) {
+      // dense box order of the L interior zones x NP pencils (SA is dead)
+      const int bi = AXIS == 0 ? p * A.L + (s - 4) : (s - 4) * NP + p;
+#pragma unroll
+      for (int f = 0; f < 8; ++f) SA[f * T + bi] = out[f];
     } else {
       const long long off = base + (long long)p * A.stride_g + (long long)s * A.stride_a;
 #pragma unroll
       for (int f = 0; f < 8; ++f) A.dst[f][off] = out[f];
+    }
+  }
+  if (tma_store) {
+    // full tile: the whole L x NP box of every field goes out with TMA
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (ci == 0) {
+      const int a0 = seg0 + 4, g = g0 + 4, o = oc + 4;
+      const int cx = AXIS == 0 ? a0 : g;
+      const int cy = AXIS == 0 ? g : (AXIS == 1 ? a0 : o);
+      const int cz = AXIS == 2 ? a0 : o;
+#pragma unroll
+      for (int f = 0; f < 8; ++f)
+        asm volatile(
+            "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::
+                "l"(reinterpret_cast<unsigned long long>(&M->out[f])),
+            "r"(cx), "r"(cy), "r"(cz), "r"(smem_u32(SA + f * T))
+            : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
     }
   }
   return tbad;
@@ -582,7 +615,7 @@ __global__ void __launch_bounds__(NP * kSweepTL, PPMLR_SWEEP_MINB)
   }
   __syncthreads();
   const bool bad = sweep_tile<AXIS, DIPOLE, NP, TLC, MainOps, kTma>(
-      A, blockIdx.x, blockIdx.y, blockIdx.z, smem, &s_err, &s_mbar);
+      A, blockIdx.x, blockIdx.y, blockIdx.z, smem, &s_err, &s_mbar, &M);
   if (__syncthreads_or(bad)) {
     if (threadIdx.x == 0)
       A.redo_list[atomicAdd(A.redo_count, 1u)] =
