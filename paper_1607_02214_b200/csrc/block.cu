@@ -520,7 +520,7 @@ int launch_sweep(ppmlr_gpu_block* b, int axis, int phase) {
   A.redo_count = b->d_redo;
   A.redo_list = b->d_redo + 1;
   const int T = slot_stride(4 * (A.L + 8));
-  const int slots = 25 + (b->with_dipole ? 3 : 0);
+  const int slots = b->with_dipole ? 28 : (PPMLR_SWEEP_XSLOTS ? 33 : 25);
   const size_t smem = sizeof(double) * (size_t)T * slots;
   // The sweep writes only the interior of the output buffer; its ghost
   // shells stay stale until the next fill (every reader fills first).

@@ -48,6 +48,9 @@ constexpr int kSweepTL = 72;
 #ifndef PPMLR_SWEEP_TMA_STORE
 #define PPMLR_SWEEP_TMA_STORE 1  // TMA stores of whole tiles' results
 #endif
+#ifndef PPMLR_SWEEP_XSLOTS
+#define PPMLR_SWEEP_XSLOTS 1  // 8 more slots without the dipole: 2 fewer barriers
+#endif
 #ifndef PPMLR_SWEEP_CSLOPE
 #define PPMLR_SWEEP_CSLOPE 1  // conserved slopes once per cell (P7b) vs per moving edge
 #endif
@@ -206,6 +209,10 @@ __device__ __forceinline__ bool sweep_tile(const SweepArgs& A, const int seg, co
   double* CF = smem + 16 * T;
   double* SA = smem + 17 * T;
   double* BD = smem + 25 * T;
+  // XS (no dipole, 33 slots): traced left states and later the slivers get
+  // their own slots TR, so neither waits for a write-after-read barrier
+  constexpr bool XS = !DIPOLE && PPMLR_SWEEP_XSLOTS;
+  double* TR = smem + 25 * T;
   const int SS = AXIS == 0 ? 1 : NP;
 
   const int nn = A.n + 8;
@@ -334,6 +341,33 @@ __device__ __forceinline__ bool sweep_tile(const SweepArgs& A, const int seg, co
     l = avg_left(al, ar, six, hs, tw);
     r = avg_right(al, ar, six, hs, tw);
   };
+  if (XS) {
+    // rho and p first (they decide the fallback), then every variable:
+    // L straight into TR, R held and written after one barrier
+    double R[8];
+    if (z3) {
+      double Lr, Lp;
+      trace(kRho, Lr, R[kRho]);
+      trace(kPE, Lp, R[kPE]);
+      badL = !(Lr > 0.0) || !(Lp > 0.0);
+      badR = !(R[kRho] > 0.0) || !(R[kPE] > 0.0);
+#pragma unroll
+      for (int v = 0; v < 8; ++v) {
+        double l = v == kRho ? Lr : Lp;
+        if (v != kRho && v != kPE) trace(v, l, R[v]);
+        const double own = PRIM[v * T + ci];
+        if (badL) l = own;
+        if (badR) R[v] = own;
+        TR[v * T + ci] = l;
+      }
+      tbad |= o3.bad;
+    }
+    __syncthreads();
+    if (z3) {
+#pragma unroll
+      for (int v = 0; v < 8; ++v) PRIM[v * T + ci] = R[v];
+    }
+  } else {
   {
     const int H[4] = {kRho, kPE, kUn, kUt1};
     double L[4], R[4];
@@ -385,12 +419,13 @@ __device__ __forceinline__ bool sweep_tile(const SweepArgs& A, const int seg, co
       }
     }
   }
+  }
   __syncthreads();
 
   // ---- P4: edge solve at m in [3, zmax] ---------------------------------
   if (live && s >= 3 && s <= zmax) {
     double f[8], bl[3] = {0.0, 0.0, 0.0}, br[3] = {0.0, 0.0, 0.0};
-    const SmemVec ql{PRIM + ci - SS, T}, qr{SA + ci, T};
+    const SmemVec ql{PRIM + ci - SS, T}, qr{(XS ? TR : SA) + ci, T};
     if (DIPOLE) {
 #pragma unroll
       for (int j = 0; j < 3; ++j) {
@@ -504,12 +539,21 @@ __device__ __forceinline__ bool sweep_tile(const SweepArgs& A, const int seg, co
       tbad |= o.bad;
     }
   }
-  __syncthreads();
-  if (e8) {
+  if (XS) {  // TR (left states) is dead since P4: no write-after-read hazard
+    if (e8) {
 #pragma unroll
-    for (int v = 0; v < 8; ++v) CONS[v * T + ci] = sl[v];
+      for (int v = 0; v < 8; ++v) TR[v * T + ci] = sl[v];
+    }
+    __syncthreads();
+  } else {
+    __syncthreads();
+    if (e8) {
+#pragma unroll
+      for (int v = 0; v < 8; ++v) CONS[v * T + ci] = sl[v];
+    }
+    __syncthreads();
   }
-  __syncthreads();
+  const double* SL = XS ? TR : CONS;  // slivers
 
   // ---- P9: remap, cons_to_prim, store (zones [4, TLv-5]) ----------------
   if (live && s >= 4 && s <= TLv - 5) {
@@ -521,7 +565,7 @@ __device__ __forceinline__ bool sweep_tile(const SweepArgs& A, const int seg, co
     const double scale = o.div(width, dxe, r_dxe);
 #pragma unroll
     for (int v = 0; v < 8; ++v)
-      u[v] = PRIM[v * T + ci] * scale + o.div(CONS[v * T + ci] - CONS[v * T + ci + SS], dxe, r_dxe);
+      u[v] = PRIM[v * T + ci] * scale + o.div(SL[v * T + ci] - SL[v * T + ci + SS], dxe, r_dxe);
     cs[0] = u[kRho];
     cs[1 + a] = u[kUn];
     cs[1 + b] = u[kUt1];
