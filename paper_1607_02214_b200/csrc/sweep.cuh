@@ -107,6 +107,11 @@ struct AxisMap {
   static constexpr int B = (AXIS + 1) % 3;  // reference t1 axis
 };
 
+template <bool B>
+struct FlatTag {
+  static constexpr bool value = B;
+};
+
 // Tile coordinates: segment along AXIS, group of NP pencils, other axis.
 struct TileId {
   int seg, grp, oc;
@@ -328,11 +333,19 @@ __device__ __forceinline__ bool sweep_tile(const SweepArgs& A, const int seg, co
     hs = 0.5 * sigma;
     tw = tw_of(sigma, k, o3);
   }
-  auto trace = [&](const int v, double& l, double& r) {
+  // The strip's last two zones are flat.  The fast build decides that once
+  // per zone outside the variable loops (compile-time F); the strict build
+  // keeps the test per variable (unswitching costs it registers).
+#ifdef PPMLR_FAST_MATH
+  constexpr bool kUnswitch = true;
+#else
+  constexpr bool kUnswitch = false;
+#endif
+  auto trace = [&](auto F, const int v, double& l, double& r) {
     const double* pv = PRIM + v * T + ci;
     const double av = pv[0];
     double al = av, ar = av, six = 0.0;
-    if (!flat) {
+    if (!decltype(F)::value && (kUnswitch || !flat)) {
       const double* dv = SA + v * T + ci;
       auto win = [&](int j) { return pv[j * SS]; };
       auto dwin = [&](int j) { return dv[j * SS]; };
@@ -345,21 +358,27 @@ __device__ __forceinline__ bool sweep_tile(const SweepArgs& A, const int seg, co
     // rho and p first (they decide the fallback), then every variable:
     // L straight into TR, R held and written after one barrier
     double R[8];
-    if (z3) {
+    auto all8 = [&](auto F) {
       double Lr, Lp;
-      trace(kRho, Lr, R[kRho]);
-      trace(kPE, Lp, R[kPE]);
+      trace(F, kRho, Lr, R[kRho]);
+      trace(F, kPE, Lp, R[kPE]);
       badL = !(Lr > 0.0) || !(Lp > 0.0);
       badR = !(R[kRho] > 0.0) || !(R[kPE] > 0.0);
 #pragma unroll
       for (int v = 0; v < 8; ++v) {
         double l = v == kRho ? Lr : Lp;
-        if (v != kRho && v != kPE) trace(v, l, R[v]);
+        if (v != kRho && v != kPE) trace(F, v, l, R[v]);
         const double own = PRIM[v * T + ci];
         if (badL) l = own;
         if (badR) R[v] = own;
         TR[v * T + ci] = l;
       }
+    };
+    if (z3) {
+      if (kUnswitch && flat)
+        all8(FlatTag<true>{});
+      else
+        all8(FlatTag<false>{});
       tbad |= o3.bad;
     }
     __syncthreads();
@@ -372,8 +391,13 @@ __device__ __forceinline__ bool sweep_tile(const SweepArgs& A, const int seg, co
     const int H[4] = {kRho, kPE, kUn, kUt1};
     double L[4], R[4];
     if (z3) {
+      if (kUnswitch && flat) {
 #pragma unroll
-      for (int j = 0; j < 4; ++j) trace(H[j], L[j], R[j]);
+        for (int j = 0; j < 4; ++j) trace(FlatTag<true>{}, H[j], L[j], R[j]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) trace(FlatTag<false>{}, H[j], L[j], R[j]);
+      }
       badL = !(L[0] > 0.0) || !(L[1] > 0.0);
       badR = !(R[0] > 0.0) || !(R[1] > 0.0);
       if (badL || badR) {  // rare: the zone falls back to its own state
@@ -398,8 +422,13 @@ __device__ __forceinline__ bool sweep_tile(const SweepArgs& A, const int seg, co
     const int H[4] = {kUt2, kBn, kBt1, kBt2};
     double L[4], R[4];
     if (z3) {
+      if (kUnswitch && flat) {
 #pragma unroll
-      for (int j = 0; j < 4; ++j) trace(H[j], L[j], R[j]);
+        for (int j = 0; j < 4; ++j) trace(FlatTag<true>{}, H[j], L[j], R[j]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) trace(FlatTag<false>{}, H[j], L[j], R[j]);
+      }
       if (badL || badR) {
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
