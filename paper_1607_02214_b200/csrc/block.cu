@@ -610,8 +610,10 @@ int launch_sources(ppmlr_gpu_block* b, int fuse_cfl) {
   A.redo_cap = b->redo_cap;
   CK(cudaMemsetAsync(b->d_redo, 0, sizeof(unsigned), b->stream));
   const cudaError_t e = b->precision == PPMLR_FAST
-                            ? launch_sources_fast(A, b->with_dipole, b->stream)
-                            : launch_sources_strict(A, b->with_dipole, b->stream);
+                            ? launch_sources_fast(A, b->src_maps[b->cur], b->with_dipole,
+                                                  b->stream)
+                            : launch_sources_strict(A, b->src_maps[b->cur], b->with_dipole,
+                                                    b->stream);
   if (e != cudaSuccess) return cuda_fail(e, "sources kernel launch");
   b->kernel_launches += 2;
   b->cur ^= 1;
@@ -667,6 +669,8 @@ int build_sweep_maps(ppmlr_gpu_block* b) {
   }
   b->maps = new SweepMaps[6];
   std::memset(static_cast<void*>(b->maps), 0, sizeof(SweepMaps) * 6);
+  b->src_maps = new SrcMaps[2];
+  std::memset(static_cast<void*>(b->src_maps), 0, sizeof(SrcMaps) * 2);
   const cuuint32_t l0 = b->sweep_L[0], l1 = b->sweep_L[1], l2 = b->sweep_L[2];
   const cuuint32_t obox[3][3] = {{l0, 4, 1}, {4, l1, 1}, {4, 1, l2}};
   const cuuint64_t dims[3] = {(cuuint64_t)b->S[0], (cuuint64_t)b->S[1], (cuuint64_t)b->S[2]};
@@ -689,6 +693,23 @@ int build_sweep_maps(ppmlr_gpu_block* b) {
         if (r != CUDA_SUCCESS) {
           set_error("cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
           return PPMLR_RUNTIME;
+        }
+      }
+      if (a == 0) {  // the source kernel's plane boxes (v, B', dipole)
+        SrcMaps& sm = b->src_maps[k];
+        const cuuint32_t pbox[3] = {(cuuint32_t)PPMLR_KNS::kSrcHX, (cuuint32_t)PPMLR_KNS::kSrcHY, 1};
+        for (int f = 0; f < 9; ++f) {
+          if (f >= 6 && !b->bd) break;
+          double* base = f < 6 ? b->buf[k] + (1 + f) * b->ncell : b->bd + (f - 6) * b->ncell;
+          const CUresult r = encode(&sm.f[f], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims,
+                                    strides, pbox, elem, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                    CU_TENSOR_MAP_SWIZZLE_NONE,
+                                    CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+          if (r != CUDA_SUCCESS) {
+            set_error("cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+            return PPMLR_RUNTIME;
+          }
         }
       }
       for (int f = 0; f < 8; ++f) {  // results go to the other buffer
@@ -883,6 +904,7 @@ void ppmlr_gpu_block_destroy(ppmlr_gpu_block* b) {
     cudaFree(b->ax[a].rden);
   }
   delete[] b->maps;
+  delete[] b->src_maps;
   if (b->snap_stream) cudaStreamSynchronize(b->snap_stream);
   cudaFree(b->d_snap);
   if (b->snap_stream) cudaStreamDestroy(b->snap_stream);

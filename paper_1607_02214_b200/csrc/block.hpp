@@ -46,6 +46,7 @@ struct StepGraph {
 
 namespace ppmlr_b200 {
 struct SweepMaps;
+struct SrcMaps;
 }
 
 struct ppmlr_gpu_block {
@@ -105,6 +106,7 @@ struct ppmlr_gpu_block {
   cudaEvent_t snap_ready = nullptr;
   // TMA descriptors of the sweep inputs: [source buffer][axis] (block.cu)
   ppmlr_b200::SweepMaps* maps = nullptr;
+  ppmlr_b200::SrcMaps* src_maps = nullptr;  // [source buffer]
 };
 
 namespace ppmlr_b200 {
@@ -116,8 +118,11 @@ struct SweepMaps;
 cudaError_t launch_sweep_strict(int axis, bool dipole, const SweepArgs& a, const SweepMaps& m,
                                 int threads, size_t smem, cudaStream_t st);
 struct SrcArgs;
-cudaError_t launch_sources_strict(const SrcArgs& a, bool dipole, cudaStream_t st);
-cudaError_t launch_sources_fast(const SrcArgs& a, bool dipole, cudaStream_t st);
+struct SrcMaps;
+cudaError_t launch_sources_strict(const SrcArgs& a, const SrcMaps& m, bool dipole,
+                                  cudaStream_t st);
+cudaError_t launch_sources_fast(const SrcArgs& a, const SrcMaps& m, bool dipole,
+                                cudaStream_t st);
 cudaError_t launch_sweep_fast(int axis, bool dipole, const SweepArgs& a, const SweepMaps& m,
                               int threads, size_t smem, cudaStream_t st);
 }  // namespace ppmlr_b200

@@ -2,10 +2,19 @@
 // (proj/src/stepper.cpp:119-200, 284-286) as stencil kernels, compiled once
 // per precision mode (PPMLR_KNS = strict | fast; see exact_div.cuh).
 #pragma once
+#include <cuda.h>  // CUtensorMap
+
 #include "grid_types.cuh"
 #include "ppmlr_dev.cuh"
 
 namespace ppmlr_b200 {
+
+// TMA descriptors of the source kernel's plane loads: v, B' (and the
+// dipole) of the source buffer, 3-D tensors over the padded block with the
+// box of one z plane of a tile plus its x/y halo ({34, 10, 1}).
+struct SrcMaps {
+  CUtensorMap f[9];
+};
 
 struct SrcArgs {
   Planes in, out;
@@ -232,8 +241,13 @@ __global__ void __launch_bounds__(256, 2) sources_exact_kernel(const SrcArgs A) 
 // stencil input is fetched from HBM once and its latency is overlapped.
 // SrcOps (branch-free fast paths); cells whose guards fail are queued for
 // sources_exact_kernel.
-constexpr int kSrcTX = 32, kSrcTY = 8, kSrcHX = kSrcTX + 2, kSrcHY = kSrcTY + 2;
+// The plane box spans x0-2 .. x0+33: a TMA box must start on a 16-byte
+// boundary in x (an even FP64 coordinate), so the x halo is 2 cells wide on
+// the left (only x0-1 is read) and 2 on the right.
+constexpr int kSrcTX = 32, kSrcTY = 8, kSrcHX = kSrcTX + 4, kSrcHY = kSrcTY + 2;
 constexpr int kSrcSlots = 4;
+// plane-field stride in the ring, padded to 128 B (the TMA destination rule)
+constexpr int kSrcPL = ((kSrcHX * kSrcHY + 15) / 16) * 16;
 
 __device__ __forceinline__ void cp_async8(double* dst, const double* src) {
   const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
@@ -246,11 +260,12 @@ __device__ __forceinline__ void cp_async_wait() {
 }
 
 template <bool DIPOLE>
-__global__ void __launch_bounds__(kSrcTX * kSrcTY, 3) sources_tiled_kernel(const SrcArgs A,
-                                                                            int zchunk) {
+__global__ void __launch_bounds__(kSrcTX * kSrcTY, 3)
+    sources_tiled_kernel(const SrcArgs A, int zchunk, const __grid_constant__ SrcMaps M) {
   constexpr int NF = DIPOLE ? 9 : 6;
-  constexpr int PL = kSrcHX * kSrcHY;  // cells per plane (incl. halo)
-  extern __shared__ double ring[];     // [kSrcSlots][NF][PL]
+  constexpr int PL = kSrcPL;                       // ring stride per plane field
+  extern __shared__ __align__(128) double ring[];  // [kSrcSlots][NF][PL]
+  __shared__ __align__(8) unsigned long long s_bar[kSrcSlots];
   const Lay& L = A.L;
   const KC c = make_kc(A.c);
   const int tx = threadIdx.x % kSrcTX, ty = threadIdx.x / kSrcTX;
@@ -262,33 +277,56 @@ __global__ void __launch_bounds__(kSrcTX * kSrcTY, 3) sources_tiled_kernel(const
   const double dt = *A.ctx.dt;
   double mn = __longlong_as_double(kInfBits);
 
-  // planes z in [z0-1, z1] exist (the ghost layer at -1 / n2 included)
-  auto issue_plane = [&](int z) {
+  // Planes z in [z0-1, z1] exist (the ghost layer at -1 / n2 included).
+  // Plane z lives in ring slot r % 4, r = z - (z0 - 1); one elected thread
+  // streams it in with TMA (one box per field) completing on that slot's
+  // mbarrier, whose phase for plane z is (r / 4) & 1.
+  auto slot_of = [&](int z) { return ring + (size_t)((z - z0 + 1) % kSrcSlots) * NF * PL; };
+  auto bar_of = [&](int z) {
+    return (unsigned)__cvta_generic_to_shared(&s_bar[(z - z0 + 1) % kSrcSlots]);
+  };
+  auto issue_plane = [&](int z) {  // thread 0 only
     if (z > z1) return;
-    double* dstp = ring + (size_t)(((z % kSrcSlots) + kSrcSlots) % kSrcSlots) * NF * PL;
-    for (int c2 = threadIdx.x; c2 < PL; c2 += blockDim.x) {
-      const int xx = c2 % kSrcHX, yy = c2 / kSrcHX;
-      const bool corner = (xx == 0 || xx == kSrcHX - 1) && (yy == 0 || yy == kSrcHY - 1);
-      if (corner) continue;
-      const long long d = L.idx(x0 - 1 + xx, y0 - 1 + yy, z);
+    const unsigned bar = bar_of(z);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                 "r"((unsigned)(NF * kSrcHX * kSrcHY * sizeof(double)))
+                 : "memory");
+    double* dstp = slot_of(z);
 #pragma unroll
-      for (int f = 0; f < 6; ++f) cp_async8(dstp + f * PL + c2, A.in.f[1 + f] + d);
-      if (DIPOLE) {
-        cp_async8(dstp + 6 * PL + c2, A.bd0 + d);
-        cp_async8(dstp + 7 * PL + c2, A.bd1 + d);
-        cp_async8(dstp + 8 * PL + c2, A.bd2 + d);
-      }
-    }
+    for (int f = 0; f < NF; ++f)
+      asm volatile(
+          "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+          " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+              (unsigned)__cvta_generic_to_shared(dstp + f * PL)),
+          "l"(reinterpret_cast<unsigned long long>(&M.f[f])), "r"(x0 - 2 + kG),
+          "r"(y0 - 1 + kG), "r"(z + kG), "r"(bar)
+          : "memory");
   };
-  auto slot_of = [&](int z) {
-    return ring + (size_t)(((z % kSrcSlots) + kSrcSlots) % kSrcSlots) * NF * PL;
+  auto wait_plane = [&](int z) {
+    const unsigned bar = bar_of(z), parity = ((z - z0 + 1) / kSrcSlots) & 1;
+    unsigned done = 0;
+    while (!done)
+      asm volatile(
+          "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; "
+          "selp.b32 %0, 1, 0, p; }"
+          : "=r"(done)
+          : "r"(bar), "r"(parity)
+          : "memory");
   };
-  issue_plane(z0 - 1);
-  cp_async_commit();
-  issue_plane(z0);
-  cp_async_commit();
-  issue_plane(z0 + 1);
-  cp_async_commit();
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < kSrcSlots; ++q)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(
+                       (unsigned)__cvta_generic_to_shared(&s_bar[q]))
+                   : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    issue_plane(z0 - 1);
+    issue_plane(z0);
+    issue_plane(z0 + 1);
+  }
+  __syncthreads();
+  wait_plane(z0 - 1);
+  wait_plane(z0);
   // per-thread constant geometry along x and y
   double hm[3], hp[3], den[3], rden[3];
   if (in_xy) {
@@ -301,7 +339,7 @@ __global__ void __launch_bounds__(kSrcTX * kSrcTY, 3) sources_tiled_kernel(const
     den[1] = A.den1[j + kG];
     rden[1] = A.rden1[j + kG];
   }
-  const int cc = (ty + 1) * kSrcHX + (tx + 1);  // this cell in a plane
+  const int cc = (ty + 1) * kSrcHX + (tx + 2);  // this cell in a plane
   double rho_n = 0.0, p_n = 0.0;                // own rho, p of plane k (prefetched)
   if (in_xy) {
     const long long d = L.idx(i, j, z0);
@@ -309,10 +347,9 @@ __global__ void __launch_bounds__(kSrcTX * kSrcTY, 3) sources_tiled_kernel(const
     p_n = A.in.f[7][d];
   }
   for (int k = z0; k < z1; ++k) {
-    issue_plane(k + 2);
-    cp_async_commit();
-    cp_async_wait<1>();  // planes <= k+1 have landed
-    __syncthreads();
+    // the end-of-iteration barrier freed plane k-2's slot for plane k+2
+    if (threadIdx.x == 0) issue_plane(k + 2);
+    wait_plane(k + 1);
     const double rho_k = rho_n, p_k = p_n;
     if (in_xy && k + 1 < z1) {
       const long long dn = L.idx(i, j, k + 1);
@@ -367,7 +404,6 @@ __global__ void __launch_bounds__(kSrcTX * kSrcTY, 3) sources_tiled_kernel(const
     }
     __syncthreads();  // plane k-1's slot is refilled next iteration
   }
-  cp_async_wait<0>();
   if (A.fuse_cfl) block_min_commit(mn, A.ctx.min);
 }
 
