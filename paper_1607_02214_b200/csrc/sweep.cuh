@@ -51,6 +51,13 @@ constexpr int kSweepTL = 72;
 #ifndef PPMLR_SWEEP_XSLOTS
 #define PPMLR_SWEEP_XSLOTS 1  // 8 more slots without the dipole: 2 fewer barriers
 #endif
+#ifndef PPMLR_SWEEP_EDGE_ONCE
+#ifdef PPMLR_FAST_MATH
+#define PPMLR_SWEEP_EDGE_ONCE 0  // measured: a wash in the fast build (more smem traffic)
+#else
+#define PPMLR_SWEEP_EDGE_ONCE 1  // strict build: interface values once per edge (+3%)
+#endif
+#endif
 #ifndef PPMLR_SWEEP_CSLOPE
 #define PPMLR_SWEEP_CSLOPE 1  // conserved slopes once per cell (P7b) vs per moving edge
 #endif
@@ -311,12 +318,87 @@ __device__ __forceinline__ bool sweep_tile(const SweepArgs& A, const int seg, co
   __syncthreads();
 
   // ---- P3: prim parabolas -> traced states (zones [2, zmax]) ------------
+  // ---- P2 (without the dipole): the CW84 interface value of every zone's
+  // right edge, once per edge (zone s+1 reads it as its left edge) -> TR
+  const bool z3 = live && s >= 2 && s <= zmax;
+  const bool flat = q >= nn - 2;  // q >= 2 always here
+  constexpr bool EO = XS && PPMLR_SWEEP_EDGE_ONCE;
+  if (EO) {
+    if (live && s >= 1 && s <= zmax && q <= nn - 3) {
+      double e[5];
+#pragma unroll
+      for (int j = 0; j < 5; ++j) e[j] = __ldg(A.qfc + 5 * (q + 1) + j);
+#pragma unroll
+      for (int v = 0; v < 8; ++v) {
+        const double* pv = PRIM + v * T + ci;
+        const double* dv = SA + v * T + ci;
+        TR[v * T + ci] = interface_value(pv[0], pv[SS], dv[0], dv[SS], e);
+      }
+    }
+    __syncthreads();
+    // ---- P3: limiter + traced states per zone from its two edge values;
+    // every read is the zone's own (PRIM, TR of s and s-1), so L goes to SA
+    // and R to PRIM at once, with no write-after-read barrier
+    if (z3) {
+      Ops o;
+      const double sigma =
+          sclamp(o.div(CF[ci] * dt, __ldg(A.dx + q), __ldg(A.rdx + q)), 0.0, 1.0);
+      const double hs = 0.5 * sigma;
+      const double tw = tw_of(sigma, k, o);
+      // the fast build decides the flat strip-end zones once per zone
+#ifdef PPMLR_FAST_MATH
+      constexpr bool kUnswitchX = true;
+#else
+      constexpr bool kUnswitchX = false;
+#endif
+      auto tr = [&](auto F, const int v, double& l, double& r) {
+        const double av = PRIM[v * T + ci];
+        double al = av, ar = av, six = 0.0;
+        if (!decltype(F)::value && (kUnswitchX || !flat)) {
+          al = TR[v * T + ci - SS];
+          ar = TR[v * T + ci];
+          limit_parabola(al, ar, av, six, k, o);
+        }
+        l = avg_left(al, ar, six, hs, tw);
+        r = avg_right(al, ar, six, hs, tw);
+      };
+      auto all8 = [&](auto F) {
+        // rho and p first: they decide the reference's fallback for all eight
+        double Lr, Rr, Lp, Rp;
+        tr(F, kRho, Lr, Rr);
+        tr(F, kPE, Lp, Rp);
+        const bool badL = !(Lr > 0.0) || !(Lp > 0.0);
+        const bool badR = !(Rr > 0.0) || !(Rp > 0.0);
+#pragma unroll
+        for (int v = 0; v < 8; ++v) {
+          double l, r;
+          if (v == kRho) {
+            l = Lr;
+            r = Rr;
+          } else if (v == kPE) {
+            l = Lp;
+            r = Rp;
+          } else {
+            tr(F, v, l, r);
+          }
+          const double own = PRIM[v * T + ci];
+          SA[v * T + ci] = badL ? own : l;
+          PRIM[v * T + ci] = badR ? own : r;
+        }
+      };
+      if (kUnswitchX && flat)
+        all8(FlatTag<true>{});
+      else
+        all8(FlatTag<false>{});
+      tbad |= o.bad;
+    }
+    __syncthreads();
+  } else {
+  // ---- P3: prim parabolas -> traced states (zones [2, zmax]) ------------
   // Two halves of four variables, each written back after a barrier, so
   // that only eight traced values are held across a barrier.  The first
   // half holds rho and p, which decide the reference's fallback to the
   // zone's own state for all eight.
-  const bool z3 = live && s >= 2 && s <= zmax;
-  const bool flat = q >= nn - 2;  // q >= 2 always here
   double e0[5], e1[5], hs = 0.0, tw = 0.0;
   bool badL = false, badR = false;
   Ops o3;
@@ -354,6 +436,7 @@ __device__ __forceinline__ bool sweep_tile(const SweepArgs& A, const int seg, co
     l = avg_left(al, ar, six, hs, tw);
     r = avg_right(al, ar, six, hs, tw);
   };
+  {
   if (XS) {
     // rho and p first (they decide the fallback), then every variable:
     // L straight into TR, R held and written after one barrier
@@ -451,10 +534,14 @@ __device__ __forceinline__ bool sweep_tile(const SweepArgs& A, const int seg, co
   }
   __syncthreads();
 
+  }
+  }
+
   // ---- P4: edge solve at m in [3, zmax] ---------------------------------
   if (live && s >= 3 && s <= zmax) {
     double f[8], bl[3] = {0.0, 0.0, 0.0}, br[3] = {0.0, 0.0, 0.0};
-    const SmemVec ql{PRIM + ci - SS, T}, qr{(XS ? TR : SA) + ci, T};
+    // traced left states: TR in the fast extra-slot schedule, else SA
+    const SmemVec ql{PRIM + ci - SS, T}, qr{((XS && !EO) ? TR : SA) + ci, T};
     if (DIPOLE) {
 #pragma unroll
       for (int j = 0; j < 3; ++j) {
