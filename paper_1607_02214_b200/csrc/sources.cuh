@@ -176,7 +176,8 @@ template <bool DIPOLE>
 __device__ __forceinline__ void source_epilogue(const SrcArgs& A, const KC& c, int i, int j,
                                                 int k, long long t, const double* s,
                                                 const double* bo, double* q, int bad,
-                                                unsigned long long step, double& mn) {
+                                                unsigned long long step, double& mn,
+                                                double d0, double d1, double d2) {
   const Lay& L = A.L;
   if (bad) {
     atomicMin(A.ctx.err, err_key(step, kPhaseSources, 0,
@@ -200,8 +201,7 @@ __device__ __forceinline__ void source_epilogue(const SrcArgs& A, const KC& c, i
   for (int f = 0; f < 8; ++f) A.out.f[f][d] = q[f];
   if (A.fuse_cfl) {
     int badax = 0;
-    if (!cfl_cell(q, bo[0], bo[1], bo[2], A.dx0[i + kG], A.dx1[j + kG], A.dx2[k + kG], c, mn,
-                  badax))
+    if (!cfl_cell(q, bo[0], bo[1], bo[2], d0, d1, d2, c, mn, badax))
       atomicMin(A.ctx.err, err_key(step + 1, kPhaseCfl, 0, ((unsigned long long)t * 3 + badax) << 2));
   }
 }
@@ -228,7 +228,8 @@ __global__ void __launch_bounds__(256, 2) sources_exact_kernel(const SrcArgs A) 
     gather_stencil<DIPOLE>(A, i, j, k, s, bo, nv, nbd, hm, hp, den, rden);
     ExactOps eo;
     const int bad = source_update(s, bo, nv, nbd, hm, hp, den, rden, c, dt, eo, q);
-    source_epilogue<DIPOLE>(A, c, i, j, k, t, s, bo, q, bad, step, mn);
+    source_epilogue<DIPOLE>(A, c, i, j, k, t, s, bo, q, bad, step, mn, A.dx0[i + kG],
+                            A.dx1[j + kG], A.dx2[k + kG]);
   }
   if (A.fuse_cfl) block_min_commit(mn, A.ctx.min);
 }
@@ -340,6 +341,10 @@ __global__ void __launch_bounds__(kSrcTX * kSrcTY, 3)
     rden[1] = A.rden1[j + kG];
   }
   const int cc = (ty + 1) * kSrcHX + (tx + 2);  // this cell in a plane
+  // per-thread spacings and the z-geometry of the plane, one plane ahead
+  const double dxi = in_xy ? A.dx0[i + kG] : 0.0, dxj = in_xy ? A.dx1[j + kG] : 0.0;
+  double gn[5] = {A.hm2[z0 + kG], A.hp2[z0 + kG], A.den2[z0 + kG], A.rden2[z0 + kG],
+                  A.dx2[z0 + kG]};
   double rho_n = 0.0, p_n = 0.0;                // own rho, p of plane k (prefetched)
   if (in_xy) {
     const long long d = L.idx(i, j, z0);
@@ -351,6 +356,16 @@ __global__ void __launch_bounds__(kSrcTX * kSrcTY, 3)
     if (threadIdx.x == 0) issue_plane(k + 2);
     wait_plane(k + 1);
     const double rho_k = rho_n, p_k = p_n;
+    double gk[5];
+#pragma unroll
+    for (int g = 0; g < 5; ++g) gk[g] = gn[g];
+    if (k + 1 < z1) {
+      gn[0] = A.hm2[k + 1 + kG];
+      gn[1] = A.hp2[k + 1 + kG];
+      gn[2] = A.den2[k + 1 + kG];
+      gn[3] = A.rden2[k + 1 + kG];
+      gn[4] = A.dx2[k + 1 + kG];
+    }
     if (in_xy && k + 1 < z1) {
       const long long dn = L.idx(i, j, k + 1);
       rho_n = A.in.f[0][dn];
@@ -388,10 +403,10 @@ __global__ void __launch_bounds__(kSrcTX * kSrcTY, 3)
         nbd[2][0][f] = DIPOLE ? pm[(6 + f) * PL + cc] : 0.0;
         nbd[2][1][f] = DIPOLE ? pp[(6 + f) * PL + cc] : 0.0;
       }
-      hm[2] = A.hm2[k + kG];
-      hp[2] = A.hp2[k + kG];
-      den[2] = A.den2[k + kG];
-      rden[2] = A.rden2[k + kG];
+      hm[2] = gk[0];
+      hp[2] = gk[1];
+      den[2] = gk[2];
+      rden[2] = gk[3];
       SrcOps fo;
       const int bad = source_update(s, bo, nv, nbd, hm, hp, den, rden, c, dt, fo, q);
       const long long t = (long long)i + (long long)L.n0 * ((long long)j + (long long)L.n1 * k);
@@ -399,7 +414,7 @@ __global__ void __launch_bounds__(kSrcTX * kSrcTY, 3)
         const unsigned slot = atomicAdd(A.redo_count, 1u);
         if (slot < A.redo_cap) A.redo_list[slot] = (unsigned)t;
       } else {
-        source_epilogue<DIPOLE>(A, c, i, j, k, t, s, bo, q, bad, step, mn);
+        source_epilogue<DIPOLE>(A, c, i, j, k, t, s, bo, q, bad, step, mn, dxi, dxj, gk[4]);
       }
     }
     __syncthreads();  // plane k-1's slot is refilled next iteration
