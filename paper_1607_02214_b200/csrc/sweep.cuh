@@ -211,7 +211,7 @@ __device__ __forceinline__ bool sweep_tile(const SweepArgs& A, const int seg, co
                                            const int oc, double* smem,
                                            unsigned long long* s_err,
                                            unsigned long long* mbar = nullptr,
-                                           const SweepMaps* M = nullptr) {
+                                           int* store = nullptr) {
   bool tbad = false;
   const int TL = TLC > 0 ? TLC : A.L + 8;
   const int NT = NP * TL;          // cells of the tile
@@ -709,23 +709,16 @@ __device__ __forceinline__ bool sweep_tile(const SweepArgs& A, const int seg, co
     }
   }
   if (tma_store) {
-    // full tile: the whole L x NP box of every field goes out with TMA
+    // whole tile: the caller sends the L x NP box of every field out with
+    // TMA after its closing barrier (the stores' smem writes are made
+    // visible to the async proxy here)
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    __syncthreads();
-    if (ci == 0) {
+    if (store) {
       const int a0 = seg0 + 4, g = g0 + 4, o = oc + 4;
-      const int cx = AXIS == 0 ? a0 : g;
-      const int cy = AXIS == 0 ? g : (AXIS == 1 ? a0 : o);
-      const int cz = AXIS == 2 ? a0 : o;
-#pragma unroll
-      for (int f = 0; f < 8; ++f)
-        asm volatile(
-            "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::
-                "l"(reinterpret_cast<unsigned long long>(&M->out[f])),
-            "r"(cx), "r"(cy), "r"(cz), "r"(smem_u32(SA + f * T))
-            : "memory");
-      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      store[0] = 1;
+      store[1] = AXIS == 0 ? a0 : g;
+      store[2] = AXIS == 0 ? g : (AXIS == 1 ? a0 : o);
+      store[3] = AXIS == 2 ? a0 : o;
     }
   }
   return tbad;
@@ -774,15 +767,35 @@ __global__ void __launch_bounds__(NP * kSweepTL, PPMLR_SWEEP_MINB)
     }
   }
   __syncthreads();
+  int store[4] = {0, 0, 0, 0};
   const bool bad = sweep_tile<AXIS, DIPOLE, NP, TLC, MainOps, kTma>(
-      A, blockIdx.x, blockIdx.y, blockIdx.z, smem, &s_err, &s_mbar, &M);
-  if (__syncthreads_or(bad)) {
+      A, blockIdx.x, blockIdx.y, blockIdx.z, smem, &s_err, &s_mbar, store);
+  // one closing barrier: the tile's results are in shared memory and its
+  // flags are final
+  const bool any_bad = __syncthreads_or(bad);
+  if (threadIdx.x == 0 && store[0]) {
+    // a flagged tile is re-run and rewritten by the exact instance later in
+    // stream order, so its box may go out regardless
+#pragma unroll
+    for (int f = 0; f < 8; ++f)
+      asm volatile(
+          "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+              reinterpret_cast<unsigned long long>(&M.out[f])),
+          "r"(store[1]), "r"(store[2]), "r"(store[3]),
+          "r"(smem_u32(smem + 17 * slot_stride(NP * (TLC > 0 ? TLC : A.L + 8)) +
+                       f * slot_stride(NP * (TLC > 0 ? TLC : A.L + 8))))
+          : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  }
+  if (any_bad) {
     if (threadIdx.x == 0)
       A.redo_list[atomicAdd(A.redo_count, 1u)] =
           blockIdx.x + A.nseg * (blockIdx.y + A.ngroups * blockIdx.z);
   } else if (threadIdx.x == 0 && s_err != kNoError) {
     atomicMin(A.err, s_err);
   }
+  // the shared memory must outlive the stores' reads of it
+  if (threadIdx.x == 0 && store[0]) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 
 }  // namespace PPMLR_KNS
