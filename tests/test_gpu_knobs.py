@@ -1,0 +1,83 @@
+"""The knobs that reach the hot path (SURVEY.md §8(b) knob table) against
+the live reference build, bit for bit in strict mode: pressure floor, ghost
+width (results must not depend on it; only the ledger does), staged
+transport, sources off, and the fast build on the same knobs within the
+stated tolerance."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import bits_equal, rel_errors
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif("not __import__('pyoracle').have_ref()")]
+
+
+def _blast_specs(n):
+    return [(-0.5, 0.5, -0.5, 0.5, 1.0 / n, n, 1.05)] * 3
+
+
+def _pair(gpu, oracle, specs, part, ic, steps, precision="strict", **kw):
+    from paper_1607_02214_b200.api import AxisSpec, HarnessOptions
+    ref = oracle.RefHarness(specs, part, **kw)
+    ref.init_ic(*ic)
+    opts = {k: v for k, v in kw.items() if k != "transport"}
+    if "boundary" in opts:
+        opts["boundary"] = {0: gpu.OUTFLOW, 1: gpu.PERIODIC, 2: gpu.MAGNETOSPHERE}[opts["boundary"]]
+    h = gpu.Harness([AxisSpec(*s) for s in specs], part,
+                    HarnessOptions(precision=precision,
+                                   transport="staged" if kw.get("transport", 1) == 0
+                                   else "direct", **opts))
+    h.init_with(*ic)
+    for _ in range(steps):
+        ref.advance()
+    h.run(steps)
+    return h, ref
+
+
+def test_pressure_floor_bitwise(gpu, oracle):
+    """pressure_floor > 0 disables the Lagrangian checks and floors p
+    (physics.cpp:40-55, ppm1d.cpp:184): a strong blast into near vacuum."""
+    h, ref = _pair(gpu, oracle, _blast_specs(24), (1, 1, 1), (gpu.IC_BLAST, (100.0, 1e-4, 0.2)),
+                   6, pressure_floor=1e-3)
+    assert bits_equal(h.gather_interior(), ref.gather())
+    assert h.time() == ref.time()
+
+
+@pytest.mark.parametrize("ghost", [5, 6])
+def test_ghost_width_changes_only_the_ledger(gpu, oracle, ghost):
+    h, ref = _pair(gpu, oracle, _blast_specs(16), (2, 1, 1), (gpu.IC_SMOOTH, ()), 4,
+                   ghost=ghost)
+    assert bits_equal(h.gather_interior(), ref.gather())
+    assert h.ledger() == ref.ledger()
+
+
+def test_staged_transport_and_no_sources(gpu, oracle):
+    h, ref = _pair(gpu, oracle, _blast_specs(16), (2, 1, 1), (gpu.IC_PARTITION, ()), 5,
+                   transport=0, with_sources=False)
+    assert bits_equal(h.gather_interior(), ref.gather())
+    assert h.ledger() == ref.ledger()
+    assert h.ledger_csv() == ref.ledger_csv()
+
+
+def test_fast_build_on_the_floor_within_tolerance(gpu, oracle):
+    h, ref = _pair(gpu, oracle, _blast_specs(24), (1, 1, 1), (gpu.IC_BLAST, (100.0, 1e-4, 0.2)),
+                   6, precision="fast", pressure_floor=1e-3)
+    l1, linf = rel_errors(h.gather_interior(), ref.gather())
+    assert np.all(l1 <= 1e-11) and np.all(linf <= 1e-9), (l1, linf)
+
+
+def test_gpu_sweep_strips_with_floor_bitwise(gpu, oracle):
+    rng = np.random.default_rng(11)
+    n, g = 40, 4
+    st = np.zeros((3, n + 2 * g, 8))
+    st[..., 0] = rng.uniform(0.5, 1.5, st.shape[:2])
+    st[..., 1] = rng.uniform(-0.5, 0.5, st.shape[:2])
+    st[..., 7] = rng.uniform(1e-6, 1e-4, st.shape[:2])
+    dx = np.full(n + 2 * g, 1.0 / n)
+    want = st.copy()
+    for k in range(3):
+        oracle.ref_sweep_1d(want[k], None, dx, n, g, 0.002, 0, pressure_floor=1e-3)
+    got = gpu.sweep_strips(st.copy(), None, dx, n, g, 0.002, 0, pressure_floor=1e-3)
+    assert bits_equal(got, want)
