@@ -332,6 +332,11 @@ def bench_e2e(h, cfg, args, cells):
     host_out = torch.empty((nz, ny, nx, 8), dtype=torch.float64, pin_memory=True).numpy()
     blk = h.block(0)
     k = args.steps
+    # one untimed pass through the same calls (first-touch costs of the
+    # transfer paths), then the timed one
+    blk.upload(host_in, st["bd"], st["frozen_idx"], st["frozen_states"])
+    h.advance()
+    blk.download_interior(out=host_out)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     blk.upload(host_in, st["bd"], st["frozen_idx"], st["frozen_states"])
@@ -343,7 +348,8 @@ def bench_e2e(h, cfg, args, cells):
     d2h = host_out.nbytes + 8 * k
     return {"value": cells * k / (t1 - t0), "unit": UNIT,
             "h2d_bytes_per_step": h2d / k, "d2h_bytes_per_step": d2h / k,
-            "how": f"upload(pinned) + {k} x advance() + download_interior(pinned), wall clock"}
+            "how": f"upload(pinned) + {k} x advance() + download_interior(pinned), wall "
+                   "clock, after one untimed pass"}
 
 
 def bench_reference(args):

@@ -640,6 +640,7 @@ int launch_step_end(ppmlr_gpu_block* b, double cfl, int close_step, int have_min
 
 namespace ppmlr_b200 {
 int block_set_dt(ppmlr_gpu_block* b, double dt) {
+  b->dt_valid = false;  // state or dt slot changes
   if (dt < 0.0) return 0;  // use the device slot as is
   b->h_pinned[1] = dt;
   CK(cudaMemcpyAsync(b->d_dt, &b->h_pinned[1], 8, cudaMemcpyHostToDevice, b->stream));
@@ -1063,6 +1064,7 @@ int block_upload_streamed(ppmlr_gpu_block* b, const ChunkFill& fill, bool with_b
 
 // Pre-filled sunward shell, fresh error window and step counter.
 int block_finish_upload(ppmlr_gpu_block* b) {
+  b->dt_valid = false;  // state or dt slot changes
   const Lay L = lay_of(b);
   // Magnetosphere: constant sunward shell in both buffers.
   if (b->boundary == PPMLR_BC_MAGNETOSPHERE && b->physical[0][1]) {
@@ -1178,13 +1180,24 @@ int ppmlr_gpu_block_snapshot_read(ppmlr_gpu_block* b, int field, int k0, int nk,
   return 0;
 }
 
-int ppmlr_gpu_block_check(ppmlr_gpu_block* b) {
+// defer_next_cfl: a non-finite CFL candidate that the fused pass found for
+// the step after the window belongs to the next advance (the reference
+// raises it from compute_global_dt at the top of that step): keep it out of
+// this result and let the next run's standalone CFL pass raise it.
+static int check_impl(ppmlr_gpu_block* b, bool defer_next_cfl) {
   CK(cudaSetDevice(b->device));
-  CK(cudaMemcpyAsync(b->h_pinned, b->d_err, 8, cudaMemcpyDeviceToHost, b->stream));
+  CK(cudaMemcpyAsync(b->h_pinned + 4, b->d_err, 16, cudaMemcpyDeviceToHost, b->stream));
   CK(cudaStreamSynchronize(b->stream));
-  unsigned long long key;
-  std::memcpy(&key, b->h_pinned, 8);
+  unsigned long long key, step;
+  std::memcpy(&key, b->h_pinned + 4, 8);
+  std::memcpy(&step, b->h_pinned + 5, 8);
   if (key == kNoError) return 0;
+  b->dt_valid = false;
+  if (defer_next_cfl && (int)((key >> 43) & 7) == kPhaseCfl && (key >> 46) == (step & 0x3FFFFull)) {
+    const unsigned long long reset = kNoError;
+    cudaMemcpy(b->d_err, &reset, 8, cudaMemcpyHostToDevice);
+    return 0;
+  }
   std::string msg;
   const int rc = decode_error(b, key, msg);
   set_error(msg);
@@ -1192,6 +1205,8 @@ int ppmlr_gpu_block_check(ppmlr_gpu_block* b) {
   cudaMemcpy(b->d_err, &reset, 8, cudaMemcpyHostToDevice);
   return rc;
 }
+
+int ppmlr_gpu_block_check(ppmlr_gpu_block* b) { return check_impl(b, false); }
 
 static int deferred(ppmlr_gpu_block* b) {
   if (b->deferred_code) {
@@ -1202,16 +1217,18 @@ static int deferred(ppmlr_gpu_block* b) {
 }
 
 int ppmlr_gpu_block_compute_dt(ppmlr_gpu_block* b, double cfl, double* dt_out) {
+  b->dt_valid = false;  // state or dt slot changes
   CK(cudaSetDevice(b->device));
   if (int rc = launch_cfl(b, 0)) return rc;
   if (int rc = launch_step_end(b, cfl, 0, 1)) return rc;
   CK(cudaMemcpyAsync(b->h_pinned + 6, b->d_dt, 8, cudaMemcpyDeviceToHost, b->stream));
-  if (int rc = ppmlr_gpu_block_check(b)) return rc;  // uses h_pinned[0]
+  if (int rc = ppmlr_gpu_block_check(b)) return rc;  // uses h_pinned[4..5]
   *dt_out = b->h_pinned[6];
   return 0;
 }
 
 int ppmlr_gpu_block_local_dt_async(ppmlr_gpu_block* b, double cfl) {
+  b->dt_valid = false;  // state or dt slot changes
   CK(cudaSetDevice(b->device));
   if (int rc = launch_cfl(b, 0)) return rc;
   return launch_step_end(b, cfl, 0, 1);
@@ -1231,6 +1248,7 @@ int ppmlr_gpu_block_fill_boundaries(ppmlr_gpu_block* b, int axis_mask, int layer
 }
 
 int ppmlr_gpu_block_sweep(ppmlr_gpu_block* b, int axis, double dt) {
+  b->dt_valid = false;  // state or dt slot changes
   CK(cudaSetDevice(b->device));
   if (axis < 0 || axis > 2) {
     set_error("sweep: axis must be 0, 1 or 2");
@@ -1246,6 +1264,7 @@ int ppmlr_gpu_block_sweep(ppmlr_gpu_block* b, int axis, double dt) {
 }
 
 int ppmlr_gpu_block_sources(ppmlr_gpu_block* b, double dt) {
+  b->dt_valid = false;  // state or dt slot changes
   CK(cudaSetDevice(b->device));
   if (int rc = block_set_dt(b, dt)) return rc;
   CK(cudaMemcpyAsync(b->buf[b->cur ^ 1], b->buf[b->cur], sizeof(double) * 8 * b->ncell,
@@ -1259,6 +1278,7 @@ int ppmlr_gpu_block_sources(ppmlr_gpu_block* b, double dt) {
 }
 
 int ppmlr_gpu_block_restore_frozen(ppmlr_gpu_block* b) {
+  b->dt_valid = false;  // state or dt slot changes
   CK(cudaSetDevice(b->device));
   return launch_frozen(b);
 }
@@ -1305,9 +1325,12 @@ static int run_steps(ppmlr_gpu_block* b, double cfl, int with_sources, long firs
     CK(cudaMemcpyAsync(b->d_err, init, sizeof init, cudaMemcpyHostToDevice, b->stream));
     b->step_base = first_step;
   }
-  // dt of the first step
-  if (int rc = launch_cfl(b, 0)) return rc;
-  if (int rc = launch_step_end(b, cfl, 0, 1)) return rc;
+  // dt of the first step, unless the previous run left it for this state
+  if (!(b->dt_valid && b->dt_cfl == cfl)) {
+    if (int rc = launch_cfl(b, 0)) return rc;
+    if (int rc = launch_step_end(b, cfl, 0, 1)) return rc;
+  }
+  b->dt_valid = false;
   const bool use_graph = !b->timing.enabled && env_int("PPMLR_NO_GRAPH", 0) == 0;
   for (long s = 0; s < steps; ++s) {
     const int parity = (first_step + s) % 2 == 0 ? 0 : 1;
@@ -1337,6 +1360,8 @@ static int run_steps(ppmlr_gpu_block* b, double cfl, int with_sources, long firs
     CK(cudaGraphLaunch(g.exec, b->stream));
     b->cur = g.cur;
   }
+  b->dt_valid = true;  // the last step's fused CFL pass computed the next dt
+  b->dt_cfl = cfl;
   return 0;
 }
 
@@ -1344,7 +1369,7 @@ int ppmlr_gpu_block_advance(ppmlr_gpu_block* b, double cfl, int with_sources, lo
                             double* dt_out) {
   if (int rc = run_steps(b, cfl, with_sources, step, 1)) return rc;
   CK(cudaMemcpyAsync(b->h_pinned + 2, b->d_dt_prev, 8, cudaMemcpyDeviceToHost, b->stream));
-  if (int rc = ppmlr_gpu_block_check(b)) return rc;
+  if (int rc = check_impl(b, true)) return rc;
   if (dt_out) *dt_out = b->h_pinned[2];
   return 0;
 }
@@ -1357,9 +1382,9 @@ int ppmlr_gpu_block_run(ppmlr_gpu_block* b, double cfl, int with_sources, long f
     CK(cudaMemcpyAsync(b->d_time, &b->h_pinned[3], 8, cudaMemcpyHostToDevice, b->stream));
   }
   if (int rc = run_steps(b, cfl, with_sources, first_step, steps)) return rc;
-  CK(cudaMemcpyAsync(b->h_pinned + 4, b->d_time, 8, cudaMemcpyDeviceToHost, b->stream));
-  if (int rc = ppmlr_gpu_block_check(b)) return rc;
-  if (time_out) *time_out = b->h_pinned[4];
+  CK(cudaMemcpyAsync(b->h_pinned + 7, b->d_time, 8, cudaMemcpyDeviceToHost, b->stream));
+  if (int rc = check_impl(b, true)) return rc;
+  if (time_out) *time_out = b->h_pinned[7];
   return 0;
 }
 
@@ -1379,6 +1404,7 @@ int ppmlr_gpu_block_pack_face(ppmlr_gpu_block* b, int face, int layers, double* 
 
 int ppmlr_gpu_block_unpack_face(ppmlr_gpu_block* b, int face, int layers,
                                 const double* dev_buf) {
+  b->dt_valid = false;  // state or dt slot changes
   CK(cudaSetDevice(b->device));
   if (face < 0 || face > 5 || layers < 1 || layers > kG) {
     set_error("unpack_face: bad face or layer count");
@@ -1394,6 +1420,7 @@ int ppmlr_gpu_block_unpack_face(ppmlr_gpu_block* b, int face, int layers,
 
 int ppmlr_gpu_block_copy_face(ppmlr_gpu_block* dst, int face, ppmlr_gpu_block* src,
                               int layers) {
+  dst->dt_valid = false;  // state or dt slot changes
   CK(cudaSetDevice(dst->device));
   const int axis = face / 2;
   if (dst->n[(axis + 1) % 3] != src->n[(axis + 1) % 3] ||
@@ -1410,6 +1437,7 @@ int ppmlr_gpu_block_copy_face(ppmlr_gpu_block* dst, int face, ppmlr_gpu_block* s
 }
 
 int ppmlr_gpu_block_begin(ppmlr_gpu_block* b, double cfl, long first_step) {
+  b->dt_valid = false;  // state or dt slot changes
   if (int rc = deferred(b)) return rc;
   CK(cudaSetDevice(b->device));
   unsigned long long init[2] = {kNoError, 0};
@@ -1420,6 +1448,7 @@ int ppmlr_gpu_block_begin(ppmlr_gpu_block* b, double cfl, long first_step) {
 }
 
 int ppmlr_gpu_block_sweep_async(ppmlr_gpu_block* b, int axis, int order_index) {
+  b->dt_valid = false;  // state or dt slot changes
   CK(cudaSetDevice(b->device));
   if (axis < 0 || axis > 2 || order_index < 0 || order_index > 2) {
     set_error("sweep_async: bad axis/order");
@@ -1429,6 +1458,7 @@ int ppmlr_gpu_block_sweep_async(ppmlr_gpu_block* b, int axis, int order_index) {
 }
 
 int ppmlr_gpu_block_end_step(ppmlr_gpu_block* b, double cfl, int with_sources) {
+  b->dt_valid = false;  // state or dt slot changes
   CK(cudaSetDevice(b->device));
   if (with_sources) {
     if (int rc = launch_sources(b, 1)) return rc;

@@ -107,6 +107,11 @@ struct ppmlr_gpu_block {
   // TMA descriptors of the sweep inputs: [source buffer][axis] (block.cu)
   ppmlr_b200::SweepMaps* maps = nullptr;
   ppmlr_b200::SrcMaps* src_maps = nullptr;  // [source buffer]
+  // The last run/advance left the next step's dt (cfl * fused CFL min of
+  // the current state) in the device slot: the next run skips its
+  // standalone CFL pass.  Any other state change clears it.
+  bool dt_valid = false;
+  double dt_cfl = 0.0;
 };
 
 namespace ppmlr_b200 {

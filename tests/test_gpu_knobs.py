@@ -81,3 +81,25 @@ def test_gpu_sweep_strips_with_floor_bitwise(gpu, oracle):
         oracle.ref_sweep_1d(want[k], None, dx, n, g, 0.002, 0, pressure_floor=1e-3)
     got = gpu.sweep_strips(st.copy(), None, dx, n, g, 0.002, 0, pressure_floor=1e-3)
     assert bits_equal(got, want)
+
+
+def test_cached_dt_is_dropped_when_the_state_changes(gpu):
+    """run/advance leave the next dt on the device and skip the next
+    standalone CFL pass; any upload must invalidate it."""
+    from paper_1607_02214_b200.api import AxisSpec, HarnessOptions
+    specs = [AxisSpec(*s) for s in _blast_specs(16)]
+    a = gpu.Harness(specs, (1, 1, 1), HarnessOptions())
+    a.init_with(gpu.IC_BLAST, (10.0, 0.1, 0.2))
+    a.run(2)
+    a.init_with(gpu.IC_SMOOTH, ())          # new state: the cached dt is stale
+    dts = [a.advance() for _ in range(3)]
+    b = gpu.Harness(specs, (1, 1, 1), HarnessOptions())
+    b.init_with(gpu.IC_SMOOTH, ())
+    want = [b.advance() for _ in range(3)]
+    assert dts == want
+    assert bits_equal(a.gather_interior(), b.gather_interior())
+    c = gpu.Harness(specs, (1, 1, 1), HarnessOptions())
+    c.init_with(gpu.IC_SMOOTH, ())
+    c.run(3)                                 # one window: same dts, same state
+    assert bits_equal(c.gather_interior(), want_state := b.gather_interior())
+    assert c.time() == b.time()
