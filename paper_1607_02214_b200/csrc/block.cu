@@ -1014,8 +1014,20 @@ int block_upload_streamed(ppmlr_gpu_block* b, const ChunkFill& fill, bool with_b
   // src_fields given: copy straight from the caller's buffers (pinned
   // memory DMAs at full PCIe rate); otherwise fill pinned staging chunks
   const bool direct = src_fields != nullptr;
-  double* host[2] = {nullptr, nullptr};
-  cudaEvent_t done[2] = {nullptr, nullptr};
+  struct Staging {  // released on every exit path (CK returns, a throwing fill)
+    cudaStream_t st;
+    double* host[2] = {nullptr, nullptr};
+    cudaEvent_t done[2] = {nullptr, nullptr};
+    ~Staging() {
+      cudaStreamSynchronize(st);
+      for (int k = 0; k < 2; ++k) {
+        if (host[k]) cudaFreeHost(host[k]);
+        if (done[k]) cudaEventDestroy(done[k]);
+      }
+    }
+  } stg{b->stream};
+  double** host = stg.host;
+  cudaEvent_t* done = stg.done;
   for (int q = 0; q < 2; ++q) {
     if (!direct) CK(cudaMallocHost(&host[q], chunk_doubles * sizeof(double)));
     CK(cudaEventCreateWithFlags(&done[q], cudaEventDisableTiming));
@@ -1053,12 +1065,8 @@ int block_upload_streamed(ppmlr_gpu_block* b, const ChunkFill& fill, bool with_b
     if (e == cudaSuccess) e = cudaEventRecord(done[q], b->stream);
     if (e != cudaSuccess) rc = cuda_fail(e, "streamed upload");
   }
-  cudaStreamSynchronize(b->stream);
-  for (int k = 0; k < 2; ++k) {
-    if (host[k]) cudaFreeHost(host[k]);
-    cudaEventDestroy(done[k]);
-  }
   if (rc) return rc;
+  CK(cudaStreamSynchronize(b->stream));
   return block_finish_upload(b);
 }
 
