@@ -84,6 +84,10 @@ def build_oracle():
     """CPU checkers (test infrastructure): oracle/liboracle.so always,
     oracle/_ref/libppmlr_ref.so when /root/reference is present."""
     _run(["make", "-C", os.path.join(ROOT, "oracle"), "-j8", "all"])
+    # the C++ drop-in check (tests/dropin): the reference's RunConfig drives
+    # ppmlr::Harness and the GPU binding side by side
+    if os.path.exists(OUT):
+        _run(["make", "-C", os.path.join(ROOT, "tests", "dropin"), "all"])
 
 
 def build_all(force=False):
