@@ -451,10 +451,15 @@ __device__ __forceinline__ bool sweep_tile(const SweepArgs& A, const int seg, co
       for (int v = 0; v < 8; ++v) {
         double l = v == kRho ? Lr : Lp;
         if (v != kRho && v != kPE) trace(F, v, l, R[v]);
-        const double own = PRIM[v * T + ci];
-        if (badL) l = own;
-        if (badR) R[v] = own;
         TR[v * T + ci] = l;
+      }
+      if (badL || badR) {  // rare: the zone falls back to its own state
+#pragma unroll
+        for (int v = 0; v < 8; ++v) {
+          const double own = PRIM[v * T + ci];  // PRIM is rewritten after the barrier
+          if (badL) TR[v * T + ci] = own;
+          if (badR) R[v] = own;
+        }
       }
     };
     if (z3) {
