@@ -520,7 +520,12 @@ int launch_sweep(ppmlr_gpu_block* b, int axis, int phase) {
   A.redo_count = b->d_redo;
   A.redo_list = b->d_redo + 1;
   const int T = slot_stride(4 * (A.L + 8));
-  const int slots = b->with_dipole ? 28 : (PPMLR_SWEEP_XSLOTS ? 33 : 25);
+  // shared slots per cell: 25 (+3 dipole), 33 with the extra-slot schedule
+  // (sweep.cuh XS; with the dipole only in the strict build)
+  const bool xs = PPMLR_SWEEP_XSLOTS &&
+                  (!b->with_dipole ||
+                   (b->precision == PPMLR_FAST ? PPMLR_SWEEP_XSD_FAST : PPMLR_SWEEP_XSD_STRICT));
+  const int slots = xs ? 33 : (b->with_dipole ? 28 : 25);
   const size_t smem = sizeof(double) * (size_t)T * slots;
   // The sweep writes only the interior of the output buffer; its ghost
   // shells stay stale until the next fill (every reader fills first).

@@ -51,6 +51,18 @@ constexpr int kSweepTL = 72;
 #ifndef PPMLR_SWEEP_XSLOTS
 #define PPMLR_SWEEP_XSLOTS 1  // 8 more slots without the dipole: 2 fewer barriers
 #endif
+// the extra-slot schedule with the dipole, per build
+#ifndef PPMLR_SWEEP_XSD_FAST
+#define PPMLR_SWEEP_XSD_FAST 0    // measured -2.7% (P4's global dipole loads)
+#endif
+#ifndef PPMLR_SWEEP_XSD_STRICT
+#define PPMLR_SWEEP_XSD_STRICT 1  // enables the edge-once trace (+0.5%)
+#endif
+#ifdef PPMLR_FAST_MATH
+#define PPMLR_SWEEP_XSLOTS_DIPOLE PPMLR_SWEEP_XSD_FAST
+#else
+#define PPMLR_SWEEP_XSLOTS_DIPOLE PPMLR_SWEEP_XSD_STRICT
+#endif
 #ifndef PPMLR_SWEEP_EDGE_ONCE
 #ifdef PPMLR_FAST_MATH
 #define PPMLR_SWEEP_EDGE_ONCE 0  // measured: a wash in the fast build (more smem traffic)
@@ -223,7 +235,10 @@ __device__ __forceinline__ bool sweep_tile(const SweepArgs& A, const int seg, co
   double* BD = smem + 25 * T;
   // XS (no dipole, 33 slots): traced left states and later the slivers get
   // their own slots TR, so neither waits for a write-after-read barrier
-  constexpr bool XS = !DIPOLE && PPMLR_SWEEP_XSLOTS;
+  // With the dipole too: its three planes land in TR[0..2] (the same slots
+  // the BD region would take), P0 reads them, and P4 takes the two cells'
+  // dipole from global memory (L2) instead of a shared BD region.
+  constexpr bool XS = PPMLR_SWEEP_XSLOTS && (!DIPOLE || PPMLR_SWEEP_XSLOTS_DIPOLE);
   double* TR = smem + 25 * T;
   const int SS = AXIS == 0 ? 1 : NP;
 
@@ -274,9 +289,11 @@ __device__ __forceinline__ bool sweep_tile(const SweepArgs& A, const int seg, co
       b0 = TMA ? BD[ci] : __ldg(A.bd[0] + off);
       b1 = TMA ? BD[T + ci] : __ldg(A.bd[1] + off);
       b2 = TMA ? BD[2 * T + ci] : __ldg(A.bd[2] + off);
-      BD[0 * T + ci] = AXIS == 0 ? b0 : (AXIS == 1 ? b1 : b2);
-      BD[1 * T + ci] = AXIS == 0 ? b1 : (AXIS == 1 ? b2 : b0);
-      BD[2 * T + ci] = AXIS == 0 ? b2 : (AXIS == 1 ? b0 : b1);
+      if (!XS) {
+        BD[0 * T + ci] = AXIS == 0 ? b0 : (AXIS == 1 ? b1 : b2);
+        BD[1 * T + ci] = AXIS == 0 ? b1 : (AXIS == 1 ? b2 : b0);
+        BD[2 * T + ci] = AXIS == 0 ? b2 : (AXIS == 1 ? b0 : b1);
+      }
     }
     double w[8];
     w[kRho] = qv[0];
@@ -547,7 +564,16 @@ __device__ __forceinline__ bool sweep_tile(const SweepArgs& A, const int seg, co
     double f[8], bl[3] = {0.0, 0.0, 0.0}, br[3] = {0.0, 0.0, 0.0};
     // traced left states: TR in the fast extra-slot schedule, else SA
     const SmemVec ql{PRIM + ci - SS, T}, qr{((XS && !EO) ? TR : SA) + ci, T};
-    if (DIPOLE) {
+    if (DIPOLE && XS) {  // strip order (a, b, d) of the zones either side
+      const long long off = base + (long long)p * A.stride_g + (long long)s * A.stride_a;
+      constexpr int ja = AXIS, jb = (AXIS + 1) % 3, jd = (AXIS + 2) % 3;
+      br[0] = __ldg(A.bd[ja] + off);
+      br[1] = __ldg(A.bd[jb] + off);
+      br[2] = __ldg(A.bd[jd] + off);
+      bl[0] = __ldg(A.bd[ja] + off - A.stride_a);
+      bl[1] = __ldg(A.bd[jb] + off - A.stride_a);
+      bl[2] = __ldg(A.bd[jd] + off - A.stride_a);
+    } else if (DIPOLE) {
 #pragma unroll
       for (int j = 0; j < 3; ++j) {
         bl[j] = BD[j * T + ci - SS];
