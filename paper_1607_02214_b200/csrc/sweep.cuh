@@ -4,31 +4,38 @@
 //
 // Work decomposition.  A CTA owns a tile of NP = 4 adjacent pencils x one
 // segment of TL = L + 8 strip positions (L interior cells plus the 4-cell
-// dependency halo on each side), one cell per thread.  The
-// tile is staged in shared memory, structure-of-arrays, and the 1-D
-// algorithm runs as cell-parallel phases separated by __syncthreads():
+// dependency halo on each side), one cell per thread.  One
+// elected thread streams the tile in with TMA (one box per field plane,
+// completing on an mbarrier); the tile is staged in shared memory,
+// structure-of-arrays, and the 1-D algorithm runs as cell-parallel phases
+// separated by __syncthreads():
 //
-//   P0  load; strip-frame prim, cons, c_f                      -> PRIM, CONS, CF
+//   P0  strip-frame prim, cons, c_f from the TMA'd fields       -> PRIM, CONS, CF
 //   P1  primitive slopes (once per cell)                        -> SA
+//   P2  (edge-once schedule) interface value per edge           -> TR
 //   P3  per zone: interface values, limited parabola, traced
-//       edge states, in two halves of four variables (each
-//       written after a barrier)                                -> PRIM:=R, SA:=L
+//       edge states                                             -> PRIM:=R, SA|TR:=L
 //   P4  per edge: Lagrangian Riemann solve                      -> CF:=u*, SA:=flux
 //   P7  per zone: Lagrangian update + the reference's checks    -> PRIM:=lag
 //   P7b tiles with a moving edge: conserved slopes per cell     -> SA
 //   P8  per moving edge only: the upwind zone's conserved
-//       parabola and the remap sliver (written after a barrier) -> CONS:=sliver
-//   P9  per zone: remap onto the fixed mesh, cons_to_prim, store
+//       parabola and the remap sliver                           -> CONS|TR:=sliver
+//   P9  per zone: remap onto the fixed mesh, cons_to_prim; whole
+//       tiles leave through TMA box stores, partial ones per thread
 //
-// 25 shared FP64 slots per cell (+3 with the dipole): 57.6 KB for the 288-cell
-// tile, 3 CTAs per SM at <= 72 registers.  Results are bit-identical to the
-// reference in the strict build: every output is produced by the
-// reference's own expression sequence; the reorganisations are exact
-// (hoisted geometry, slivers and sigma terms evaluated once per edge instead
-// of twice, conserved slopes recomputed per moving edge, segment halos
-// recomputed).  Arithmetic goes through an Ops policy (exact_div.cuh): the
-// main instance runs branch-free fast paths and flags tiles whose guards
-// failed; the EXACT instance re-runs those tiles with plain `/` and `sqrt`.
+// Shared FP64 slots per cell: 25 (+3 with the dipole) = 57.6 KB for the
+// 288-cell tile, or 33 (the extra-slot schedule XS: TR) = 76 KB; 3 CTAs per
+// SM at <= 72 registers either way.  XS lets the traced left states and the
+// slivers skip a write-after-read barrier; its edge-once variant (EO,
+// strict build) computes each interface value once.  Results are
+// bit-identical to the reference in the strict build: every output is
+// produced by the reference's own expression sequence; the reorganisations
+// are exact (hoisted geometry, interface values / slivers / sigma terms
+// evaluated once per edge instead of twice, conserved slopes per cell only
+// where the tile moves, segment halos recomputed).  Arithmetic goes through
+// an Ops policy (exact_div.cuh): the main instance runs branch-free fast
+// paths and flags tiles whose guards failed; the EXACT instance re-runs
+// those tiles with plain `/` and `sqrt`.
 #pragma once
 #include <cuda.h>  // CUtensorMap (the maps are encoded on the host, block.cu)
 
