@@ -137,6 +137,16 @@ def fp64_peak_tflops(device=0):
 
 # ------------------------------------------------------------ CPU baseline
 
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def cpu_baseline(kind_cfg, seconds_target=12.0, threads=None):
     """The reference's own CPU implementation (oracle/_ref, built from the
     unmodified sources) on a bounded sample of the workload, one independent
@@ -162,7 +172,10 @@ def cpu_baseline(kind_cfg, seconds_target=12.0, threads=None):
         rate, secs = po.ref_bench(specs, ic[0], ic[1], threads, steps, **kw)
         return {"value": rate, "unit": UNIT, "cores": threads, "kind": "reference",
                 "sample": f"{sample}; {steps} steps x {threads} threads in {secs:.1f} s "
-                          f"(oracle/_ref: unmodified reference sources, g++ -O3)"}
+                          f"(oracle/_ref: unmodified reference sources, g++ -O3)",
+                "single_core": {"value": r1, "unit": UNIT,
+                                "sample": "the calibration step: 1 step, 1 thread"},
+                "cpu_model": _cpu_model()}
     return cpu_baseline_port(kind_cfg, seconds_target, threads)
 
 
