@@ -655,6 +655,10 @@ int block_set_dt(ppmlr_gpu_block* b, double dt) {
 
 // ---------------------------------------------------------------- C-ABI
 
+#ifndef PPMLR_TMA_L2_PROMOTION
+#define PPMLR_TMA_L2_PROMOTION CU_TENSOR_MAP_L2_PROMOTION_L2_256B  // measured +0.5-0.8%
+#endif
+
 namespace {
 // TMA descriptors of the sweep inputs for both ping-pong buffers and every
 // axis: each field / dipole plane as a 3-D tensor {S0, S1, S2} (x pitch P0)
@@ -694,7 +698,7 @@ int build_sweep_maps(ppmlr_gpu_block* b) {
         CUtensorMap* t = f < 8 ? &m.f[f] : &m.bd[f - 8];
         const CUresult r = encode(t, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides,
                                   box[a], elem, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                                  CU_TENSOR_MAP_SWIZZLE_NONE, PPMLR_TMA_L2_PROMOTION,
                                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) {
           set_error("cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
@@ -710,7 +714,7 @@ int build_sweep_maps(ppmlr_gpu_block* b) {
           const CUresult r = encode(&sm.f[f], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims,
                                     strides, pbox, elem, CU_TENSOR_MAP_INTERLEAVE_NONE,
                                     CU_TENSOR_MAP_SWIZZLE_NONE,
-                                    CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                                    PPMLR_TMA_L2_PROMOTION,
                                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
           if (r != CUDA_SUCCESS) {
             set_error("cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
