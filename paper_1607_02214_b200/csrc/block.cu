@@ -483,7 +483,7 @@ void choose_sweep_tiles(ppmlr_gpu_block* b) {
 namespace ppmlr_b200 {
 
 int launch_sweep(ppmlr_gpu_block* b, int axis, int phase) {
-  SweepArgs A;
+  SweepArgs A{};
   double* in = b->buf[b->cur];
   double* out = b->buf[b->cur ^ 1];
   for (int f = 0; f < 8; ++f) {
