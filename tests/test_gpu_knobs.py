@@ -103,3 +103,32 @@ def test_cached_dt_is_dropped_when_the_state_changes(gpu):
     c.run(3)                                 # one window: same dts, same state
     assert bits_equal(c.gather_interior(), want_state := b.gather_interior())
     assert c.time() == b.time()
+
+
+@pytest.mark.parametrize("dims,boundary,ic", [
+    ((17, 13, 11), 0, (3, (10.0, 0.1, 0.3))),   # odd sizes: partial tiles, OOB boxes
+    ((67, 9, 130), 0, (4, ())),                 # one long axis (runtime tile), odd short ones
+    ((36, 20, 12), 1, (4, ())),                 # periodic
+    ((257, 6, 5), 0, (5, ())),                  # > 256 cells: the compile-time tile, partial tail
+])
+def test_odd_sizes_bitwise_vs_reference(gpu, oracle, dims, boundary, ic):
+    specs = [(-1.0, 1.0, -1.0, 1.0, 2.0 / n, n, 1.05) for n in dims]
+    h, ref = _pair(gpu, oracle, specs, (1, 1, 1), ic, 4, boundary=boundary)
+    assert bits_equal(h.gather_interior(), ref.gather())
+    assert h.time() == ref.time()
+
+
+def test_odd_sizes_magnetosphere_partitioned(gpu, oracle):
+    from paper_1607_02214_b200.api import AxisSpec, HarnessOptions
+    specs = [(-48.0, 28.8, -48.0, 28.8, 1.2, 64, 1.05),
+             (-22.8, 22.8, -22.8, 22.8, 1.2, 38, 1.05),
+             (-20.4, 20.4, -20.4, 20.4, 1.2, 34, 1.05)]
+    ref = oracle.RefHarness(specs, (2, 1, 1), boundary=2, with_dipole=True)
+    ref.init_magnetosphere()
+    h = gpu.Harness([AxisSpec(*s) for s in specs], (2, 1, 1),
+                    HarnessOptions(boundary=gpu.MAGNETOSPHERE, with_dipole=True))
+    h.init_magnetosphere()
+    for _ in range(4):
+        ref.advance()
+    h.run(4)
+    assert bits_equal(h.gather_interior(), ref.gather())
