@@ -132,3 +132,24 @@ def test_odd_sizes_magnetosphere_partitioned(gpu, oracle):
         ref.advance()
     h.run(4)
     assert bits_equal(h.gather_interior(), ref.gather())
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("cfg,steps", [("ot512", 100), ("briowu", 220)])
+def test_fast_build_long_runs_within_tolerance(gpu, cfg, steps):
+    """BASELINE configs C2 (Orszag-Tang 512x512x4, L1 error vs the CPU
+    reference after 100 steps) and C1 (Brio-Wu 256x4x4 to t~0.1, 220 steps):
+    the fast build against the strict build, which is bit-identical to the
+    reference."""
+    from dataclasses import replace
+    from paper_1607_02214_b200 import configs
+    c = configs.orszag_tang(n=512) if cfg == "ot512" else configs.brio_wu()
+    out = {}
+    for prec in ("strict", "fast"):
+        h = gpu.Harness(c.specs, c.partition, replace(c.options, precision=prec))
+        configs.init(h, c)
+        h.run(steps)
+        out[prec] = h.gather_interior()
+    l1, linf = rel_errors(out["fast"], out["strict"])
+    print(cfg, "rel L1", l1.max(), "rel Linf", linf.max())
+    assert np.all(l1 <= 1e-11) and np.all(linf <= 1e-9), (l1, linf)
