@@ -1301,26 +1301,33 @@ int ppmlr_gpu_block_restore_frozen(ppmlr_gpu_block* b) {
 }
 
 // One full step of a whole-domain block, stream-ordered, dt already in d_dt.
+// A sweep launch bracketed by CUDA events when timing is on (the dominant
+// kernel's in-run duration for bench.py's roofline).
+static int timed_sweep(ppmlr_gpu_block* b, int axis, int phase) {
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (b->timing.enabled) {
+    auto& t = b->timing;
+    while (t.pool.size() < t.used + 2) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      t.pool.push_back(e);
+    }
+    e0 = t.pool[t.used];
+    e1 = t.pool[t.used + 1];
+    t.used += 2;
+    CK(cudaEventRecord(e0, b->stream));
+  }
+  if (int rc = launch_sweep(b, axis, phase)) return rc;
+  if (e1) CK(cudaEventRecord(e1, b->stream));
+  return 0;
+}
+
 static int enqueue_step(ppmlr_gpu_block* b, double cfl, int with_sources, int parity) {
   static const int order[2][3] = {{0, 1, 2}, {2, 1, 0}};
   for (int s = 0; s < 3; ++s) {
     const int axis = order[parity][s];
     if (int rc = launch_bc(b, 1 << axis, kG)) return rc;
-    cudaEvent_t e0 = nullptr, e1 = nullptr;
-    if (b->timing.enabled) {
-      auto& t = b->timing;
-      while (t.pool.size() < t.used + 2) {
-        cudaEvent_t e;
-        CK(cudaEventCreate(&e));
-        t.pool.push_back(e);
-      }
-      e0 = t.pool[t.used];
-      e1 = t.pool[t.used + 1];
-      t.used += 2;
-      CK(cudaEventRecord(e0, b->stream));
-    }
-    if (int rc = launch_sweep(b, axis, kPhaseSweep0 + s)) return rc;
-    if (e1) CK(cudaEventRecord(e1, b->stream));
+    if (int rc = timed_sweep(b, axis, kPhaseSweep0 + s)) return rc;
   }
   if (with_sources) {
     if (int rc = launch_bc(b, 7, 1)) return rc;
@@ -1471,7 +1478,7 @@ int ppmlr_gpu_block_sweep_async(ppmlr_gpu_block* b, int axis, int order_index) {
     set_error("sweep_async: bad axis/order");
     return PPMLR_INVALID_SPEC;
   }
-  return launch_sweep(b, axis, kPhaseSweep0 + order_index);
+  return timed_sweep(b, axis, kPhaseSweep0 + order_index);
 }
 
 int ppmlr_gpu_block_end_step(ppmlr_gpu_block* b, double cfl, int with_sources) {

@@ -144,16 +144,20 @@ class DeviceRankBlock:
         self.device = device
         check(N.lib.ppmlr_gpu_block_set_stream(h, C.c_void_p(
             torch.cuda.current_stream(device).cuda_stream)))
-        fi = st["frozen_idx"]
-        check(N.lib.ppmlr_gpu_block_upload(
-            h, st["fields"].ctypes.data_as(C.POINTER(C.c_double)),
-            None if st["bd"] is None else st["bd"].ctypes.data_as(C.POINTER(C.c_double)),
-            fi.ctypes.data_as(C.POINTER(C.c_int64)) if len(fi) else None,
-            st["frozen_states"].ctypes.data_as(C.POINTER(C.c_double)) if len(fi) else None,
-            len(fi)))
+        self.upload(st["fields"], st["bd"], st["frozen_idx"], st["frozen_states"])
         self._dt = torch.as_tensor(_CudaPtr(N.lib.ppmlr_gpu_block_dt_slot(h), 1),
                                    device=f"cuda:{device}")
         self.n = self.info.n
+
+    def upload(self, fields, bd, frozen_idx, frozen_states):
+        """ghost-inclusive reference-layout state host -> device."""
+        fi = frozen_idx
+        self.check_rc(self.N.lib.ppmlr_gpu_block_upload(
+            self.h, fields.ctypes.data_as(C.POINTER(C.c_double)),
+            None if bd is None else bd.ctypes.data_as(C.POINTER(C.c_double)),
+            fi.ctypes.data_as(C.POINTER(C.c_int64)) if len(fi) else None,
+            frozen_states.ctypes.data_as(C.POINTER(C.c_double)) if len(fi) else None,
+            len(fi)))
 
     def close(self):
         if getattr(self, "h", None):
@@ -192,9 +196,10 @@ class DeviceRankBlock:
                                                         C.byref(k), C.byref(n)))
         return sw.value, k.value, n.value
 
-    def interior(self):
+    def interior(self, out=None):
         nx, ny, nz = self.n
-        out = np.zeros((nz, ny, nx, 8))
+        if out is None:
+            out = np.zeros((nz, ny, nx, 8))
         self.check_rc(self.N.lib.ppmlr_gpu_block_download_interior(
             self.h, out.ctypes.data_as(C.POINTER(C.c_double))))
         return out
@@ -205,6 +210,54 @@ def run_rank(blk, ex, steps, first_step, cfl, with_sources, group=None, dt_ready
         begin(blk, cfl, first_step, group)
     for s in range(steps):
         advance(blk, ex, first_step + s, cfl, with_sources, group)
+
+
+def _traffic(kind, cells):
+    """dram bytes of one sweep launch scaled from the committed ncu capture
+    (profiles/ncu_sweep_traffic.json), or None."""
+    prof = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                        "profiles", "ncu_sweep_traffic.json")
+    try:
+        rec = json.load(open(prof)).get(kind, {})
+        return rec["bytes_per_cell"] * cells if "bytes_per_cell" in rec else None
+    except (OSError, ValueError):
+        return None
+
+
+def _e2e_distributed(blk, ex, cfg, rank, world, args, cfl, srcs, cells_rank, local, UNIT):
+    """End to end per rank through the block API, max over ranks: the
+    rank's initial state uploaded from pinned host memory, K distributed
+    steps, the interior downloaded into pinned host memory (one untimed pass
+    first)."""
+    import torch
+    import torch.distributed as dist
+    from .api import host_block_state
+    st = host_block_state(cfg.specs, cfg.partition, cfg.options, rank, cfg.ic)
+    fin = torch.empty(st["fields"].shape, dtype=torch.float64, pin_memory=True).numpy()
+    fin[...] = st["fields"]
+    nx, ny, nz = blk.n
+    fout = torch.empty((nz, ny, nx, 8), dtype=torch.float64, pin_memory=True).numpy()
+    k = args.steps
+
+    def one(steps):
+        blk.upload(fin, st["bd"], st["frozen_idx"], st["frozen_states"])
+        run_rank(blk, ex, steps, 0, cfl, srcs)
+        blk.interior(out=fout)
+
+    one(1)
+    torch.cuda.synchronize()
+    dist.barrier()
+    t0 = time.perf_counter()
+    one(k)
+    t1 = time.perf_counter()
+    el = torch.tensor([t1 - t0], device=f"cuda:{local}", dtype=torch.float64)
+    dist.all_reduce(el, op=dist.ReduceOp.MAX)
+    h2d = fin.nbytes + (st["bd"].nbytes if st["bd"] is not None else 0)
+    return {"value": cells_rank * world * k / float(el.item()), "unit": UNIT,
+            "h2d_bytes_per_step": world * h2d / k,
+            "d2h_bytes_per_step": world * (fout.nbytes + 8 * k) / k,
+            "how": f"per rank: upload(pinned) + {k} distributed steps + "
+                   "download_interior(pinned), wall clock, max over ranks, after one untimed pass"}
 
 
 def bench_distributed(args, METRIC, UNIT, ALG, make_config, ClockSampler, fp64_peak_tflops,
@@ -248,11 +301,12 @@ def bench_distributed(args, METRIC, UNIT, ALG, make_config, ClockSampler, fp64_p
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     ms = float(ms.item())
     sweep_ms, kernels, launches = blk.timing(False)
+    e2e = _e2e_distributed(blk, ex, cfg, rank, world, args, cfl, srcs, cells_rank, local, UNIT)
     value = cells_rank * world * args.steps / (ms * 1e-3)
     if rank == 0:
         peak = fp64_peak_tflops(local)
         hbm, hbm_src = measured_peaks()
-        avg = sweep_ms * 1e-3 / max(launches, 1)
+        avg = max(sweep_ms * 1e-3 / max(launches, 1), 1e-12)
         fb = cells_rank * alg["B_sweep"] / avg / (hbm * 1e9)
         ff = cells_rank * alg["F_sweep"] / avg / (peak * 1e12)
         bound = "fp64" if ff >= fb else "hbm"
@@ -271,9 +325,10 @@ def bench_distributed(args, METRIC, UNIT, ALG, make_config, ClockSampler, fp64_p
                          else cells_rank * alg["B_sweep"] / avg / 1e9,
                          "peak": peak if bound == "fp64" else hbm,
                          "unit": "TFLOP/s" if bound == "fp64" else "GB/s",
-                         "frac": ff if bound == "fp64" else fb, "traffic": None,
+                         "frac": ff if bound == "fp64" else fb,
+                         "traffic": _traffic(kind, cells_rank),
                          "frac_hbm": fb, "frac_fp64": ff, "peak_hbm_source": hbm_src},
-            "e2e": None,
+            "e2e": e2e,
         }
         print(json.dumps(line), flush=True)
     blk.close()
