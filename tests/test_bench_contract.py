@@ -27,3 +27,39 @@ def test_reference_arm_json_line():
     assert line["cpu_baseline"]["kind"] == "reference" and line["cpu_baseline"]["cores"] >= 1
     assert line["e2e"] == {"value": line["value"], "unit": line["unit"],
                            "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
+
+
+def _run_json(cmd):
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-3000:]
+    return json.loads(out.stdout.strip().splitlines()[-1])
+
+
+KEYS = ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+        "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config", "clocks",
+        "e2e", "gpu_launches", "roofline")
+
+
+@pytest.mark.gpu
+def test_bench_line_single_gpu(gpu):
+    line = _run_json([sys.executable, os.path.join(ROOT, "bench.py"), "--config", "blast64",
+                      "--steps", "3", "--warmup", "3", "--no-cpu-baseline"])
+    for key in KEYS:
+        assert key in line, key
+    assert line["value"] > 0 and line["gpu_launches"] > 0
+    assert line["e2e"]["value"] > 0 and line["e2e"]["h2d_bytes_per_step"] > 0
+    r = line["roofline"]
+    assert r["bound"] in ("fp64", "hbm") and 0 < r["frac"] < 1
+
+
+@pytest.mark.gpu
+def test_bench_line_distributed_single_rank(gpu):
+    """The torchrun arm (one rank per GPU over NCCL) on the one visible GPU."""
+    line = _run_json([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                      "--nproc-per-node", "1", "--master-addr", "127.0.0.1", "--master-port",
+                      "29533", os.path.join(ROOT, "bench.py"), "--gpus", "1", "--config",
+                      "blast64", "--steps", "3", "--warmup", "3", "--force-dist"])
+    for key in KEYS:
+        assert key in line, key
+    assert line["value"] > 0 and line["e2e"]["value"] > 0
+    assert 0 < line["roofline"]["frac"] < 1
