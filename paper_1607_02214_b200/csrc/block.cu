@@ -454,8 +454,8 @@ void choose_sweep_tiles(ppmlr_gpu_block* b) {
   // Segments of kSweepTL - 8 = 64 cells (compile-time tile) when the axis is a
   // multiple of 64 or long enough that a partial last segment costs little;
   // otherwise balanced segments of at most Lmax cells (runtime tile).
-  // one cell per thread: a tile is at most 288 cells (L <= 64)
-  const int Lmax = std::min(env_int("PPMLR_SWEEP_LMAX", 64), kSweepTL - 8);
+  // one cell per thread: a tile is at most kSweepNP * kSweepTL cells
+  const int Lmax = std::min(env_int("PPMLR_SWEEP_LMAX", kSweepTL - 8), kSweepTL - 8);
   const int ipt = 1;
   const int Lc = kSweepTL - 8;
   for (int a = 0; a < 3; ++a) {
@@ -469,10 +469,10 @@ void choose_sweep_tiles(ppmlr_gpu_block* b) {
       L += L & 1;  // even: the x tile box row (TL doubles) must be a multiple of 16 B
     }
     b->sweep_L[a] = L;
-    const int T = 4 * (L + 8);
+    const int T = kSweepNP * (L + 8);
     int nt = (T + ipt - 1) / ipt;
     nt = ((nt + 31) / 32) * 32;
-    b->sweep_threads[a] = std::min(4 * kSweepTL, std::max(32, nt));
+    b->sweep_threads[a] = std::min(kSweepNP * kSweepTL, std::max(32, nt));
   }
 }
 
@@ -507,7 +507,7 @@ int launch_sweep(ppmlr_gpu_block* b, int axis, int phase) {
   A.nb = b->n[(axis + 1) % 3];
   A.L = b->sweep_L[axis];
   A.nseg = (A.n + A.L - 1) / A.L;
-  A.ngroups = (A.ng + 3) / 4;
+  A.ngroups = (A.ng + kSweepNP - 1) / kSweepNP;
   if (A.ngroups > 65535 || A.no > 65535) {  // grid (nseg, ngroups, no)
     set_error("sweep: too many pencils across the sweep axis for one launch grid");
     return PPMLR_INVALID_SPEC;
@@ -519,7 +519,7 @@ int launch_sweep(ppmlr_gpu_block* b, int axis, int phase) {
   A.c = b->c;
   A.redo_count = b->d_redo;
   A.redo_list = b->d_redo + 1;
-  const int T = slot_stride(4 * (A.L + 8));
+  const int T = slot_stride(kSweepNP * (A.L + 8));
   // shared slots per cell: 25 (+3 dipole), 33 with the extra-slot schedule
   // (sweep.cuh XS; with the dipole only in the strict build)
   const bool xs = PPMLR_SWEEP_XSLOTS &&
@@ -682,13 +682,14 @@ int build_sweep_maps(ppmlr_gpu_block* b) {
   b->src_maps = new SrcMaps[2];
   std::memset(static_cast<void*>(b->src_maps), 0, sizeof(SrcMaps) * 2);
   const cuuint32_t l0 = b->sweep_L[0], l1 = b->sweep_L[1], l2 = b->sweep_L[2];
-  const cuuint32_t obox[3][3] = {{l0, 4, 1}, {4, l1, 1}, {4, 1, l2}};
+  const cuuint32_t np = kSweepNP;
+  const cuuint32_t obox[3][3] = {{l0, np, 1}, {np, l1, 1}, {np, 1, l2}};
   const cuuint64_t dims[3] = {(cuuint64_t)b->S[0], (cuuint64_t)b->S[1], (cuuint64_t)b->S[2]};
   const cuuint64_t strides[2] = {(cuuint64_t)b->sy * 8, (cuuint64_t)b->sz * 8};
   const cuuint32_t elem[3] = {1, 1, 1};
   // tile box per axis: TL = L + 8 strip positions x 4 pencils
   const cuuint32_t t0 = b->sweep_L[0] + 8, t1 = b->sweep_L[1] + 8, t2 = b->sweep_L[2] + 8;
-  const cuuint32_t box[3][3] = {{t0, 4, 1}, {4, t1, 1}, {4, 1, t2}};
+  const cuuint32_t box[3][3] = {{t0, np, 1}, {np, t1, 1}, {np, 1, t2}};
   for (int k = 0; k < 2; ++k)
     for (int a = 0; a < 3; ++a) {
       SweepMaps& m = b->maps[3 * k + a];
@@ -882,7 +883,7 @@ int ppmlr_gpu_block_create(const ppmlr_gpu_block_desc* d, ppmlr_gpu_block** out)
     for (int a = 0; a < 3; ++a) {
       const int G = a == 0 ? 1 : 0, O = a == 2 ? 1 : 2;
       const long long t = (long long)((b->n[a] + b->sweep_L[a] - 1) / b->sweep_L[a]) *
-                          ((b->n[G] + 3) / 4) * b->n[O];
+                          ((b->n[G] + kSweepNP - 1) / kSweepNP) * b->n[O];
       tiles = std::max(tiles, t);
     }
     const long long cells = (long long)b->n[0] * b->n[1] * b->n[2];

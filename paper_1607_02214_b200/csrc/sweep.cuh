@@ -43,9 +43,16 @@
 
 namespace ppmlr_b200 {
 
-// Compile-time tile length of the main sweep instantiation (L = 64 interior
+// Compile-time tile of the main sweep instantiation (default L = 64 interior
 // cells per segment, 4 pencils per tile).
-constexpr int kSweepTL = 72;
+#ifndef PPMLR_SWEEP_NP
+#define PPMLR_SWEEP_NP 4   // pencils per tile
+#endif
+#ifndef PPMLR_SWEEP_TL
+#define PPMLR_SWEEP_TL 72  // strip positions per tile (L + 8; even)
+#endif
+constexpr int kSweepNP = PPMLR_SWEEP_NP;
+constexpr int kSweepTL = PPMLR_SWEEP_TL;
 #ifndef PPMLR_SWEEP_MINB
 #define PPMLR_SWEEP_MINB 3  // resident CTAs per SM the register budget targets
 #endif
