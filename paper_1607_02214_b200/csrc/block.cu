@@ -950,8 +950,23 @@ namespace ppmlr_b200 {
 // Frozen inner core (init_magnetosphere, stepper.cpp:107-110): bounding-box
 // slot map + SoA states on the device; linear indices in the caller's
 // (ghost g_ref) layout.
+// Instantiated step graphs bake in kernel arguments (the frozen-core slot
+// map's pointers and bounding box among them); anything that changes those
+// must drop them so the next step re-captures.
+static void drop_step_graphs(ppmlr_gpu_block* b) {
+  for (auto& row : b->graphs)
+    for (auto& g : row)
+      if (g.exec) {
+        cudaGraphExecDestroy(g.exec);
+        g.exec = nullptr;
+      }
+}
+
 int block_set_frozen(ppmlr_gpu_block* b, const int64_t* frozen_idx, const double* frozen_states,
                      int64_t n_frozen) {
+  CK(cudaSetDevice(b->device));
+  CK(cudaStreamSynchronize(b->stream));  // no step in flight reads the old map
+  drop_step_graphs(b);
   const int gr = b->g_ref;
   const int S0r = b->n[0] + 2 * gr, S1r = b->n[1] + 2 * gr;
   const Lay L = lay_of(b);
@@ -1510,12 +1525,7 @@ int ppmlr_gpu_block_set_stream(ppmlr_gpu_block* b, void* stream) {
   if (b->own_stream) cudaStreamDestroy(b->stream);
   b->stream = static_cast<cudaStream_t>(stream);
   b->own_stream = false;
-  for (auto& row : b->graphs)
-    for (auto& g : row)
-      if (g.exec) {
-        cudaGraphExecDestroy(g.exec);
-        g.exec = nullptr;
-      }
+  drop_step_graphs(b);
   return 0;
 }
 

@@ -153,3 +153,27 @@ def test_fast_build_long_runs_within_tolerance(gpu, cfg, steps):
     l1, linf = rel_errors(out["fast"], out["strict"])
     print(cfg, "rel L1", l1.max(), "rel Linf", linf.max())
     assert np.all(l1 <= 1e-11) and np.all(linf <= 1e-9), (l1, linf)
+
+
+def test_upload_with_a_new_frozen_core_recaptures_the_step(gpu):
+    """The step graphs bake in the frozen-core slot map (pointers and
+    bounding box); an upload that replaces the frozen set must drop them.
+    A harness that already stepped, re-uploaded with a smaller frozen set,
+    must match a fresh harness given the same upload, bit for bit."""
+    from paper_1607_02214_b200 import configs
+    cfg = configs.magnetosphere_small()
+    st = gpu.host_block_state(cfg.specs, (1, 1, 1), cfg.options, 0, cfg.ic)
+    nf = len(st["frozen_idx"])
+    assert nf > 8
+    keep = slice(0, nf // 2)                 # a different frozen set and box
+    out = []
+    for warm in (True, False):
+        h = gpu.Harness(cfg.specs, (1, 1, 1), cfg.options)
+        configs.init(h, cfg)
+        if warm:
+            h.run(2)                         # step graphs captured
+        h.block(0).upload(st["fields"], st["bd"], st["frozen_idx"][keep],
+                          st["frozen_states"][keep])
+        h.run(3)
+        out.append(h.gather_interior())
+    assert bits_equal(out[0], out[1])
