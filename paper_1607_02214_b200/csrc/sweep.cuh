@@ -87,6 +87,13 @@ constexpr int kSweepTL = PPMLR_SWEEP_TL;
 #ifndef PPMLR_SWEEP_CSLOPE
 #define PPMLR_SWEEP_CSLOPE 1  // conserved slopes once per cell (P7b) vs per moving edge
 #endif
+#ifndef PPMLR_SWEEP_FUSE01
+// XS schedule with TMA'd tiles: the primitive slopes are taken in P0 from the
+// TMA'd input slots (the strip-frame primitives are a permutation of the
+// fields), into TR; P3 then writes the traced left states into SA.  One
+// barrier fewer per tile.
+#define PPMLR_SWEEP_FUSE01 1
+#endif
 
 // TMA descriptors of the sweep's input: the 8 field planes of the source
 // buffer and the 3 dipole planes, each a 3-D (x, y, z) tensor over the padded
@@ -254,6 +261,10 @@ __device__ __forceinline__ bool sweep_tile(const SweepArgs& A, const int seg, co
   // dipole from global memory (L2) instead of a shared BD region.
   constexpr bool XS = PPMLR_SWEEP_XSLOTS && (!DIPOLE || PPMLR_SWEEP_XSLOTS_DIPOLE);
   double* TR = smem + 25 * T;
+  constexpr bool F01 = PPMLR_SWEEP_FUSE01 && TMA && XS && !(XS && PPMLR_SWEEP_EDGE_ONCE);
+  // F01: slopes in TR, the traced left states in SA
+  double* SLP = F01 ? TR : SA;
+  double* LFT = F01 ? SA : TR;
   const int SS = AXIS == 0 ? 1 : NP;
 
   const int nn = A.n + 8;
@@ -333,11 +344,23 @@ __device__ __forceinline__ bool sweep_tile(const SweepArgs& A, const int seg, co
     CONS[kBt1 * T + ci] = w[kBt1];
     CONS[kBt2 * T + ci] = w[kBt2];
     CONS[kPE * T + ci] = e;
+    if (F01 && s >= 1 && s <= TLv - 2) {
+      // P1 fused: the neighbours' strip-frame primitives straight from the
+      // TMA'd fields (PRIM is a pure permutation of them) -> TR
+      const double* gc = A.slope + 3 * q;
+      const double c0 = __ldg(gc), cA = __ldg(gc + 1), cB = __ldg(gc + 2);
+      constexpr int fof[8] = {0, 1 + a, 1 + b, 1 + d, 4 + a, 4 + b, 4 + d, 7};
+#pragma unroll
+      for (int v = 0; v < 8; ++v) {
+        const double* pv = SA + fof[v] * T + ci;
+        TR[v * T + ci] = limited_slope(pv[-SS], w[v], pv[SS], c0, cA, cB);
+      }
+    }
   }
   __syncthreads();
 
   // ---- P1: primitive slopes at s in [1, TLv-2] -> SA ---------------------
-  if (live && s >= 1 && s <= TLv - 2) {
+  if (!F01 && live && s >= 1 && s <= TLv - 2) {
     const double* gc = A.slope + 3 * q;
     const double c0 = __ldg(gc), cA = __ldg(gc + 1), cB = __ldg(gc + 2);
 #pragma unroll
@@ -346,7 +369,7 @@ __device__ __forceinline__ bool sweep_tile(const SweepArgs& A, const int seg, co
       SA[v * T + ci] = limited_slope(pv[-SS], pv[0], pv[SS], c0, cA, cB);
     }
   }
-  __syncthreads();
+  if (!F01) __syncthreads();
 
   // ---- P3: prim parabolas -> traced states (zones [2, zmax]) ------------
   // ---- P2 (without the dipole): the CW84 interface value of every zone's
@@ -459,7 +482,7 @@ __device__ __forceinline__ bool sweep_tile(const SweepArgs& A, const int seg, co
     const double av = pv[0];
     double al = av, ar = av, six = 0.0;
     if (!decltype(F)::value && (kUnswitch || !flat)) {
-      const double* dv = SA + v * T + ci;
+      const double* dv = SLP + v * T + ci;
       auto win = [&](int j) { return pv[j * SS]; };
       auto dwin = [&](int j) { return dv[j * SS]; };
       zone_parabola_dm(win, dwin, e0, e1, k, o3, al, ar, six);
@@ -482,13 +505,13 @@ __device__ __forceinline__ bool sweep_tile(const SweepArgs& A, const int seg, co
       for (int v = 0; v < 8; ++v) {
         double l = v == kRho ? Lr : Lp;
         if (v != kRho && v != kPE) trace(F, v, l, R[v]);
-        TR[v * T + ci] = l;
+        LFT[v * T + ci] = l;
       }
       if (badL || badR) {  // rare: the zone falls back to its own state
 #pragma unroll
         for (int v = 0; v < 8; ++v) {
           const double own = PRIM[v * T + ci];  // PRIM is rewritten after the barrier
-          if (badL) TR[v * T + ci] = own;
+          if (badL) LFT[v * T + ci] = own;
           if (badR) R[v] = own;
         }
       }
@@ -577,7 +600,7 @@ __device__ __forceinline__ bool sweep_tile(const SweepArgs& A, const int seg, co
   if (live && s >= 3 && s <= zmax) {
     double f[8], bl[3] = {0.0, 0.0, 0.0}, br[3] = {0.0, 0.0, 0.0};
     // traced left states: TR in the fast extra-slot schedule, else SA
-    const SmemVec ql{PRIM + ci - SS, T}, qr{((XS && !EO) ? TR : SA) + ci, T};
+    const SmemVec ql{PRIM + ci - SS, T}, qr{((XS && !EO) ? LFT : SA) + ci, T};
     if (DIPOLE && XS) {  // strip order (a, b, d) of the zones either side
       const long long off = base + (long long)p * A.stride_g + (long long)s * A.stride_a;
       constexpr int ja = AXIS, jb = (AXIS + 1) % 3, jd = (AXIS + 2) % 3;
