@@ -11,6 +11,8 @@
 // separated by __syncthreads():
 //
 //   P0  strip-frame prim, cons, c_f from the TMA'd fields       -> PRIM, CONS, CF
+//       (fast XS: primitive slopes here too -> TR; PRIM left unwritten, P3
+//       reads the field slots and PRIM/SA swap roles from P4 on)
 //   P1  primitive slopes (once per cell)                        -> SA
 //   P2  (edge-once schedule) interface value per edge           -> TR
 //   P3  per zone: interface values, limited parabola, traced
@@ -94,6 +96,13 @@ constexpr int kSweepTL = PPMLR_SWEEP_TL;
 // fields), into TR; P3 then writes the traced left states into SA.  One
 // barrier fewer per tile.
 #define PPMLR_SWEEP_FUSE01 1
+#endif
+#ifndef PPMLR_SWEEP_P0NOPRIM
+// F01: P0 leaves PRIM unwritten (the TMA'd field slots in SA already hold
+// the primitives, permuted); P3 reads them there, writes the traced left
+// states to PRIM at once and the right states to SA after its barrier, and
+// from P4 on the two regions swap roles.
+#define PPMLR_SWEEP_P0NOPRIM 1
 #endif
 #ifndef PPMLR_SWEEP_FUSE7B
 // extra-slot schedules: the tile's "any moving edge" vote is taken at P4's
@@ -272,8 +281,9 @@ __device__ __forceinline__ bool sweep_tile(const SweepArgs& A, const int seg, co
   double* TR = smem + 25 * T;
   constexpr bool F01 = PPMLR_SWEEP_FUSE01 && TMA && XS && !(XS && PPMLR_SWEEP_EDGE_ONCE);
   // F01: slopes in TR, the traced left states in SA
+  constexpr bool NP0 = F01 && PPMLR_SWEEP_P0NOPRIM;
   double* SLP = F01 ? TR : SA;
-  double* LFT = F01 ? SA : TR;
+  double* LFT = NP0 ? PRIM : (F01 ? SA : TR);
   const int SS = AXIS == 0 ? 1 : NP;
   // (with the dipole, measured -0.4% on the strict magnetosphere: kept off)
   constexpr bool F7 = PPMLR_SWEEP_FUSE7B && XS && !DIPOLE && PPMLR_SWEEP_CSLOPE;
@@ -312,6 +322,8 @@ __device__ __forceinline__ bool sweep_tile(const SweepArgs& A, const int seg, co
     return (unsigned long long)t1 + (unsigned long long)A.nb * (unsigned long long)t2;
   };
   constexpr int a = AXIS, b = (AXIS + 1) % 3, d = (AXIS + 2) % 3;
+  // field slot of each strip variable (the TMA'd fields are in field order)
+  constexpr int fof[8] = {0, 1 + a, 1 + b, 1 + d, 4 + a, 4 + b, 4 + d, 7};
 
   // ---- P0 ---------------------------------------------------------------
   if (TMA) mbar_wait(mbar, 0);
@@ -345,8 +357,10 @@ __device__ __forceinline__ bool sweep_tile(const SweepArgs& A, const int seg, co
     const double e = strip_energy(w, k, o);
     tbad |= o.bad;
     CF[ci] = cf;
+    if (!NP0) {
 #pragma unroll
-    for (int v = 0; v < 8; ++v) PRIM[v * T + ci] = w[v];
+      for (int v = 0; v < 8; ++v) PRIM[v * T + ci] = w[v];
+    }
     CONS[kRho * T + ci] = w[kRho];
     CONS[kUn * T + ci] = w[kRho] * w[kUn];
     CONS[kUt1 * T + ci] = w[kRho] * w[kUt1];
@@ -360,7 +374,6 @@ __device__ __forceinline__ bool sweep_tile(const SweepArgs& A, const int seg, co
       // TMA'd fields (PRIM is a pure permutation of them) -> TR
       const double* gc = A.slope + 3 * q;
       const double c0 = __ldg(gc), cA = __ldg(gc + 1), cB = __ldg(gc + 2);
-      constexpr int fof[8] = {0, 1 + a, 1 + b, 1 + d, 4 + a, 4 + b, 4 + d, 7};
 #pragma unroll
       for (int v = 0; v < 8; ++v) {
         const double* pv = SA + fof[v] * T + ci;
@@ -489,7 +502,7 @@ __device__ __forceinline__ bool sweep_tile(const SweepArgs& A, const int seg, co
   constexpr bool kUnswitch = false;
 #endif
   auto trace = [&](auto F, const int v, double& l, double& r) {
-    const double* pv = PRIM + v * T + ci;
+    const double* pv = NP0 ? SA + fof[v] * T + ci : PRIM + v * T + ci;
     const double av = pv[0];
     double al = av, ar = av, six = 0.0;
     if (!decltype(F)::value && (kUnswitch || !flat)) {
@@ -521,7 +534,8 @@ __device__ __forceinline__ bool sweep_tile(const SweepArgs& A, const int seg, co
       if (badL || badR) {  // rare: the zone falls back to its own state
 #pragma unroll
         for (int v = 0; v < 8; ++v) {
-          const double own = PRIM[v * T + ci];  // PRIM is rewritten after the barrier
+          // PRIM (NP0: SA) is rewritten after the barrier
+          const double own = NP0 ? SA[fof[v] * T + ci] : PRIM[v * T + ci];
           if (badL) LFT[v * T + ci] = own;
           if (badR) R[v] = own;
         }
@@ -537,7 +551,13 @@ __device__ __forceinline__ bool sweep_tile(const SweepArgs& A, const int seg, co
     __syncthreads();
     if (z3) {
 #pragma unroll
-      for (int v = 0; v < 8; ++v) PRIM[v * T + ci] = R[v];
+      for (int v = 0; v < 8; ++v) (NP0 ? SA : PRIM)[v * T + ci] = R[v];
+    }
+    if (NP0) {  // from P4 on: right states (then lag values) in SA's slots
+      double* t = PRIM;
+      PRIM = SA;
+      SA = t;
+      LFT = SA;
     }
   } else {
   {
@@ -822,7 +842,7 @@ __device__ __forceinline__ bool sweep_tile(const SweepArgs& A, const int seg, co
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     if (store) {
       const int a0 = seg0 + 4, g = g0 + 4, o = oc + 4;
-      store[0] = F7 ? 25 : 17;  // first slot of the staged box
+      store[0] = (int)(OUT - smem) / T;  // first slot of the staged box
       store[1] = AXIS == 0 ? a0 : g;
       store[2] = AXIS == 0 ? g : (AXIS == 1 ? a0 : o);
       store[3] = AXIS == 2 ? a0 : o;
