@@ -95,10 +95,26 @@ class ClockSampler:
                 stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
-        time.sleep(0.3)
+        # nvidia-smi can take longer to start than a short timed region lasts
+        # (C3: 10 steps = 18 ms): wait for its first row so the region is
+        # always bracketed by samples
+        t0 = time.time()
+        while self.proc and self._rows() < 1 and time.time() - t0 < 5.0:
+            time.sleep(0.05)
+        self.n0 = self._rows()
         return self
 
+    def _rows(self):
+        try:
+            with open(self.path) as f:
+                return sum(1 for _ in f)
+        except Exception:
+            return 0
+
     def __exit__(self, *exc):
+        t0 = time.time()
+        while self.proc and self._rows() <= self.n0 and time.time() - t0 < 0.5:
+            time.sleep(0.02)
         if self.proc:
             self.proc.terminate()
             try:
