@@ -55,6 +55,32 @@ def measured_peaks():
         return HBM_FALLBACK_GBS, "fallback"
 
 
+def workload(name, gpus):
+    """(physics kind, config dict) of a bench workload, computed here without
+    importing the product package, so that the reference arm (which must not
+    load the product's native library) prints the same `config` as ours."""
+    g = max(int(gpus), 1)
+    if name.startswith("blast"):
+        n = 512 if name == "blast512" else int(name[5:])
+        kind, wl, grid = "blast", f"blast_{n}^3x{g}", [n * g, n, n]
+    elif name == "ot512":
+        kind, wl, grid = "orszag_tang", "orszag_tang", [512, 512, 4]
+    elif name == "mag160":
+        kind, wl, grid = "magnetosphere", "magnetosphere_160x150x150", [160, 150, 150]
+    elif name == "mag1024":
+        kind, wl, grid = "magnetosphere", "magnetosphere_1024x768x768", [1024, 768, 768]
+    elif name == "briowu":
+        kind, wl, grid = "briowu", "briowu", [256, 4, 4]
+    else:
+        raise SystemExit(f"unknown config {name}")
+    cells = grid[0] * grid[1] * grid[2]
+    return kind, {"workload": wl, "grid": grid, "cells_per_gpu": cells // g,
+                  "partition": f"x-slab ({g},1,1)",
+                  "l2": "inputs (2 state buffers of 8 FP64 planes) >> 126 MB L2 at the "
+                        "headline sizes; no flush needed" if cells >= 1 << 24 else
+                        "state fits L2 partly: correctness config, not a headline"}
+
+
 def make_config(name, gpus):
     from paper_1607_02214_b200 import configs
     if name == "blast512":
@@ -163,39 +189,67 @@ def _cpu_model():
     return None
 
 
-def cpu_baseline(kind_cfg, seconds_target=12.0, threads=None):
+# The bounded CPU sample of each workload: (specs, harness kwargs, ic, steps
+# per thread, whether the rate is extrapolated to the workload's size).  The
+# step count is FIXED per workload, so every CPU leg (our line's
+# cpu_baseline and the --impl reference arm) times the same sample.
+def _cpu_sample(name):
+    if name.startswith("blast"):
+        n = 64
+        return ([(-0.5, 0.5, -0.5, 0.5, 1.0 / n, n, 1.05)] * 3, dict(boundary=0),
+                (3, (10.0, 0.1, 0.1)), 24,
+                "64^3 blast unit block (the C4 IC/physics at 1/512 of the cells)", True)
+    if name in ("mag160", "mag1024"):
+        return ([(-100.0, 30.0, -10.0, 10.0, 0.4, 160, 1.05),
+                 (-100.0, 100.0, -10.0, 10.0, 0.4, 150, 1.05),
+                 (-100.0, 100.0, -10.0, 10.0, 0.4, 150, 1.05)],
+                dict(boundary=2, with_dipole=True), (-1, ()), 1,
+                "C3 160x150x150 magnetosphere (stretched grid, dipole, frozen core)",
+                name == "mag1024")
+    if name == "ot512":
+        tp = 2.0 * np.pi
+        return ([(0.0, tp, 0.0, tp, tp / 512, 512, 1.05)] * 2
+                + [(0.0, tp * 4 / 512, 0.0, tp * 4 / 512, tp / 512, 4, 1.05)],
+                dict(boundary=1), (2, (5.0 / 3.0,)), 2, "C2 Orszag-Tang 512x512x4", False)
+    if name == "briowu":
+        d = 1.0 / 256
+        return ([(0.0, 1.0, 0.0, 1.0, d, 256, 1.05), (0.0, 4 * d, 0.0, 4 * d, d, 4, 1.05),
+                 (0.0, 4 * d, 0.0, 4 * d, d, 4, 1.05)],
+                dict(boundary=0, gamma=2.0), (1, ()), 200, "C1 Brio-Wu 256x4x4", False)
+    raise SystemExit(f"unknown config {name}")
+
+
+def cpu_baseline(name, threads=None):
     """The reference's own CPU implementation (oracle/_ref, built from the
-    unmodified sources) on a bounded sample of the workload, one independent
-    harness per host thread.  Falls back to the C restatement ("port")."""
+    unmodified sources) on a bounded sample of workload `name`, one
+    independent harness per host thread, a fixed number of steps each (one
+    untimed step first).  Falls back to the C restatement ("port") when the
+    reference build is absent."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import pyoracle as po
     threads = threads or os.cpu_count() or 1
-    n = 64
-    specs = [(-0.5, 0.5, -0.5, 0.5, 1.0 / n, n, 1.05)] * 3
-    sample = f"{n}^3 blast unit block (same IC/physics as C4), one independent block per thread"
-    if kind_cfg == "magnetosphere":
-        specs = [(-100.0, 30.0, -10.0, 10.0, 0.4, 160, 1.05),
-                 (-100.0, 100.0, -10.0, 10.0, 0.4, 150, 1.05),
-                 (-100.0, 100.0, -10.0, 10.0, 0.4, 150, 1.05)]
-        sample = "C3 160x150x150 magnetosphere, one independent harness per thread"
-    if po.have_ref():
-        kw = dict(boundary=0) if kind_cfg != "magnetosphere" else dict(boundary=2,
-                                                                       with_dipole=True)
-        ic = (3, (10.0, 0.1, 0.1)) if kind_cfg != "magnetosphere" else (-1, ())
-        # calibrate: one step single-threaded
-        r1, s1 = po.ref_bench(specs, ic[0], ic[1], 1, 1, **kw)
-        steps = max(1, int(seconds_target / max(s1, 1e-3) / 2))
-        rate, secs = po.ref_bench(specs, ic[0], ic[1], threads, steps, **kw)
-        return {"value": rate, "unit": UNIT, "cores": threads, "kind": "reference",
-                "sample": f"{sample}; {steps} steps x {threads} threads in {secs:.1f} s "
-                          f"(oracle/_ref: unmodified reference sources, g++ -O3)",
-                "single_core": {"value": r1, "unit": UNIT,
-                                "sample": "the calibration step: 1 step, 1 thread"},
-                "cpu_model": _cpu_model()}
-    return cpu_baseline_port(kind_cfg, seconds_target, threads)
+    specs, kw, ic, steps, sample, extrapolated = _cpu_sample(name)
+    if not po.have_ref():
+        return cpu_baseline_port(name, threads)
+    po.ref_bench(specs, ic[0], ic[1], 1, 1, **kw)  # warm-up (page-in, caches)
+    r1, s1 = po.ref_bench(specs, ic[0], ic[1], 1, 1, **kw)
+    rate, secs = po.ref_bench(specs, ic[0], ic[1], threads, steps, **kw)
+    how = ("per-cell rate EXTRAPOLATED to the workload's size (the reference is serial "
+           "per block; cell-updates/s of the sample)" if extrapolated else
+           "the workload itself, fewer steps")
+    return {"value": rate, "unit": UNIT, "cores": threads, "kind": "reference",
+            "extrapolated": extrapolated,
+            "sample": f"{sample}: one independent harness per thread, {steps} steps x "
+                      f"{threads} threads in {secs:.1f} s; {how} (oracle/_ref: unmodified "
+                      f"reference sources, g++ -O3)",
+            "single_core": {"value": r1, "unit": UNIT, "sample": "1 step, 1 thread"},
+            "cpu_model": _cpu_model()}
 
 
-def cpu_baseline_port(kind_cfg, seconds_target, threads):
+def cpu_baseline_port(name, threads, seconds_target=10.0):
+    """Fallback without oracle/_ref: the C restatement on a 48^3 blast.  (It
+    takes the IC from the product's host planning; never used when the
+    reference build exists, as it does on the GPU box.)"""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import pyoracle as po
     from paper_1607_02214_b200 import configs, host_block_state
@@ -234,6 +288,8 @@ def bench_single(args):
     import torch
     import paper_1607_02214_b200 as P
     cfg, kind = make_config(args.config, 1)
+    _, wl_cfg = workload(args.config, 1)
+    assert wl_cfg["workload"] == cfg.name and wl_cfg["cells_per_gpu"] == cfg.cells, wl_cfg
     cfg.options.precision = args.precision
     alg = ALG[kind]
     cells = cfg.cells
@@ -337,14 +393,12 @@ def bench_single(args):
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "precision": args.precision,
         "data": "synthetic (deterministic IC, no RNG)",
-        "config": {"workload": cfg.name, "grid": [int(s.cells) for s in cfg.specs],
-                   "cells_per_gpu": cells, "partition": "x-slab (P,1,1)",
-                   "l2": "state (2 x 9 GB ping-pong) >> 126 MB L2; no flush needed"},
+        "config": wl_cfg,
         "clocks": clk.summary(), "e2e": e2e, "gpu_launches": int(kernels),
         "roofline": roofline, "other_precision": other,
     }
     if not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(kind)
+        line["cpu_baseline"] = cpu_baseline(args.config)
     print(json.dumps(line), flush=True)
 
 
@@ -382,16 +436,19 @@ def bench_e2e(h, cfg, args, cells):
 
 
 def bench_reference(args):
+    """The reference arm: the reference's own CPU implementation
+    (oracle/_ref, the unmodified sources) on the host cores, timed on the
+    same fixed sample as our line's cpu_baseline.  It never imports the
+    product package (no product native library is loaded here)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    _, kind = make_config(args.config, 1) if args.config != "mag1024" else (None,
-                                                                           "magnetosphere")
-    cb = cpu_baseline(kind, seconds_target=max(6.0, 2.0 * args.steps))
+    _, wl_cfg = workload(args.config, args.gpus)
+    cb = cpu_baseline(args.config)
     line = {"metric": METRIC, "value": cb["value"], "unit": UNIT, "impl": "reference",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": args.config},
+            "data": "synthetic (deterministic IC, no RNG)", "config": wl_cfg,
             "cpu_baseline": cb,
             "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
@@ -421,7 +478,8 @@ def main():
     if world > 1 or args.gpus > 1 or args.force_dist:
         from paper_1607_02214_b200 import dist
         return dist.bench_distributed(args, METRIC, UNIT, ALG, make_config, ClockSampler,
-                                      fp64_peak_tflops, measured_peaks, cpu_baseline)
+                                      fp64_peak_tflops, measured_peaks, cpu_baseline,
+                                      workload)
     return bench_single(args)
 
 

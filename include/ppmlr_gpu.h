@@ -194,6 +194,13 @@ int ppmlr_gpu_block_local_dt_async(ppmlr_gpu_block* b, double cfl);
 void* ppmlr_gpu_block_stream(ppmlr_gpu_block* b);
 int ppmlr_gpu_block_set_stream(ppmlr_gpu_block* b, void* stream);
 int ppmlr_gpu_block_synchronize(ppmlr_gpu_block* b);
+/* Device-resident state of the block (no copy; valid until the next call
+ * that steps or uploads): the 8 field planes (rho, vx, vy, vz, Bx', By',
+ * Bz', p) of the current buffer, each S0 x S1 x S2 ghost-inclusive with
+ * element strides (1, strides[1], strides[2]); dims = S.  Returns the device
+ * ghost width (4).  For on-device consumers (analysis, comparisons). */
+int ppmlr_gpu_block_state_view(ppmlr_gpu_block* b, double** field_planes, long long* strides,
+                               int* dims);
 /* Error word check (host sync): returns the status of the first failure
  * recorded since the last check, with the reference's message. */
 int ppmlr_gpu_block_check(ppmlr_gpu_block* b);

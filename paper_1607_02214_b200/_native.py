@@ -140,6 +140,8 @@ _sig("ppmlr_gpu_block_time", C.c_int, _BP, _dp)
 _sig("ppmlr_gpu_block_stream", _vp, _BP)
 _sig("ppmlr_gpu_block_set_stream", C.c_int, _BP, _vp)
 _sig("ppmlr_gpu_block_synchronize", C.c_int, _BP)
+_sig("ppmlr_gpu_block_state_view", C.c_int, _BP, C.POINTER(C.c_void_p),
+     C.POINTER(C.c_longlong), C.POINTER(C.c_int))
 _sig("ppmlr_gpu_block_check", C.c_int, _BP)
 _sig("ppmlr_gpu_block_timing", C.c_int, _BP, C.c_int, _dp, _dp, C.POINTER(C.c_long))
 _sig("ppmlr_gpu_sweep_strips", C.c_int, _dp, _dp, _dp, C.c_int, C.c_int, C.c_int, C.c_int,

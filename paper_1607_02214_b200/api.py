@@ -157,8 +157,9 @@ class HarnessOptions:
 class Block:
     """A device-resident BlockState (non-owning view when from a Harness)."""
 
-    def __init__(self, handle, owner=None, shape=None, ghost=4):
+    def __init__(self, handle, owner=None, shape=None, ghost=4, device=0):
         self.h = handle
+        self.device = device
         self._owner = owner
         self.shape = shape  # interior (nx, ny, nz)
         self.ghost = ghost
@@ -221,6 +222,30 @@ class Block:
 
     def synchronize(self):
         check(N.lib.ppmlr_gpu_block_synchronize(self.h))
+
+    def state_view(self, interior=True):
+        """The device-resident state as 8 torch tensors (z, y, x) viewing the
+        library's memory (no copy; valid until the next step or upload)."""
+        import torch
+        pl = (C.c_void_p * 8)()
+        st = (C.c_longlong * 3)()
+        dims = (C.c_int * 3)()
+        g = N.lib.ppmlr_gpu_block_state_view(self.h, pl, st, dims)
+        out = []
+        for f in range(8):
+            shape = (dims[2], dims[1], st[1])
+            t = torch.as_tensor(_CudaArray(pl[f], shape, (st[2] * 8, st[1] * 8, 8)),
+                                device=f"cuda:{self.device}")
+            t = t[:, :, :dims[0]]
+            out.append(t[g:-g, g:-g, g:-g] if interior else t)
+        return out
+
+
+class _CudaArray:
+    def __init__(self, ptr, shape, strides):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": "<f8",
+                                         "strides": tuple(strides),
+                                         "data": (int(ptr), False), "version": 3}
 
 
 class Harness:
@@ -293,7 +318,7 @@ class Harness:
     def block(self, rank=0):
         info = self.layout[rank]
         return Block(N.lib.ppmlr_gpu_harness_block(self.h, rank), owner=self, shape=info.n,
-                     ghost=self.options.ghost)
+                     ghost=self.options.ghost, device=self.options.device)
 
     def gather_interior(self):
         nx, ny, nz = (build_axis(s).n for s in self.specs)

@@ -361,8 +361,8 @@ double* cur_buf(ppmlr_gpu_block* b) { return b->buf[b->cur]; }
 
 // Reference message for a decoded error key (sweep / sources / CFL).
 int decode_error(ppmlr_gpu_block* b, unsigned long long key, std::string& msg) {
-  const int phase = (int)((key >> 43) & 7);
-  const unsigned long long pos = key & ((1ull << 41) - 1);
+  const int phase = err_phase(key);
+  const unsigned long long pos = err_pos(key);
   const int kind = (int)(pos & 3);
   char buf[512];
   if (phase == kPhaseCfl) {
@@ -386,7 +386,7 @@ int decode_error(ppmlr_gpu_block* b, unsigned long long key, std::string& msg) {
     msg = buf;
     return PPMLR_UNPHYSICAL;
   }
-  const int axis = (int)((key >> 41) & 3);
+  const int axis = err_axis(key);
   const unsigned long long pencil = pos >> 20;
   const int sub = (int)((pos >> 19) & 1);
   const int zone = (int)((pos >> 2) & 0x1FFFF);
@@ -762,6 +762,15 @@ int ppmlr_gpu_block_create(const ppmlr_gpu_block_desc* d, ppmlr_gpu_block** out)
     set_error("ghost width must be >= 4");
     return PPMLR_INVALID_SPEC;
   }
+  // the first-failure error keys (ppmlr_common.hpp) address strip positions
+  // in 17 bits and the pencils of a face in 27
+  for (int a = 0; a < 3; ++a)
+    if (d->n[a] + 2 * kG >= kMaxStrip ||
+        (unsigned long long)d->n[(a + 1) % 3] * d->n[(a + 2) % 3] >= kMaxPencils) {
+      set_error("block too large for the error-key fields: an axis must have fewer than "
+                "131064 cells and a face fewer than 2^27 pencils");
+      return PPMLR_INVALID_SPEC;
+    }
   int ndev = 0;
   CK(cudaGetDeviceCount(&ndev));
   if (d->device < 0 || d->device >= ndev) {
@@ -1226,7 +1235,7 @@ static int check_impl(ppmlr_gpu_block* b, bool defer_next_cfl) {
   std::memcpy(&step, b->h_pinned + 5, 8);
   if (key == kNoError) return 0;
   b->dt_valid = false;
-  if (defer_next_cfl && (int)((key >> 43) & 7) == kPhaseCfl && (key >> 46) == (step & 0x3FFFFull)) {
+  if (defer_next_cfl && err_phase(key) == kPhaseCfl && err_step(key) == (step & kErrStepMask)) {
     const unsigned long long reset = kNoError;
     cudaMemcpy(b->d_err, &reset, 8, cudaMemcpyHostToDevice);
     return 0;
@@ -1421,7 +1430,15 @@ int ppmlr_gpu_block_run(ppmlr_gpu_block* b, double cfl, int with_sources, long f
     b->h_pinned[3] = *time_out;
     CK(cudaMemcpyAsync(b->d_time, &b->h_pinned[3], 8, cudaMemcpyHostToDevice, b->stream));
   }
-  if (int rc = run_steps(b, cfl, with_sources, first_step, steps)) return rc;
+  // errors are checked at least every kMaxStepsPerCheck steps: the keys'
+  // step field counts from the start of each window and must not wrap
+  for (long done = 0; done < steps;) {
+    const long k = std::min(steps - done, kMaxStepsPerCheck);
+    if (int rc = run_steps(b, cfl, with_sources, first_step + done, k)) return rc;
+    if (done + k < steps)
+      if (int rc = check_impl(b, true)) return rc;
+    done += k;
+  }
   CK(cudaMemcpyAsync(b->h_pinned + 7, b->d_time, 8, cudaMemcpyDeviceToHost, b->stream));
   if (int rc = check_impl(b, true)) return rc;
   if (time_out) *time_out = b->h_pinned[7];
@@ -1533,6 +1550,16 @@ int ppmlr_gpu_block_synchronize(ppmlr_gpu_block* b) {
   CK(cudaSetDevice(b->device));
   CK(cudaStreamSynchronize(b->stream));
   return 0;
+}
+
+int ppmlr_gpu_block_state_view(ppmlr_gpu_block* b, double** field_planes, long long* strides,
+                               int* dims) {
+  for (int f = 0; f < 8; ++f) field_planes[f] = cur_buf(b) + (long long)f * b->ncell;
+  strides[0] = 1;
+  strides[1] = b->sy;
+  strides[2] = b->sz;
+  for (int a = 0; a < 3; ++a) dims[a] = b->S[a];
+  return kG;
 }
 
 int ppmlr_gpu_block_timing(ppmlr_gpu_block* b, int enable, double* sweep_ms, double* total_ms,

@@ -842,7 +842,7 @@ __device__ __forceinline__ bool sweep_tile(const SweepArgs& A, const int seg, co
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     if (store) {
       const int a0 = seg0 + 4, g = g0 + 4, o = oc + 4;
-      store[0] = (int)(OUT - smem) / T;  // first slot of the staged box
+      store[0] = (int)(OUT - smem) / T;  // first slot of the staged box (may be 0)
       store[1] = AXIS == 0 ? a0 : g;
       store[2] = AXIS == 0 ? g : (AXIS == 1 ? a0 : o);
       store[3] = AXIS == 2 ? a0 : o;
@@ -894,13 +894,14 @@ __global__ void __launch_bounds__(NP * kSweepTL, PPMLR_SWEEP_MINB)
     }
   }
   __syncthreads();
-  int store[4] = {0, 0, 0, 0};
+  // store[0]: first smem slot of the staged result box, -1 = no TMA store
+  int store[4] = {-1, 0, 0, 0};
   const bool bad = sweep_tile<AXIS, DIPOLE, NP, TLC, MainOps, kTma>(
       A, blockIdx.x, blockIdx.y, blockIdx.z, smem, &s_err, &s_mbar, store);
   // one closing barrier: the tile's results are in shared memory and its
   // flags are final
   const bool any_bad = __syncthreads_or(bad);
-  if (threadIdx.x == 0 && store[0]) {
+  if (threadIdx.x == 0 && store[0] >= 0) {
     // a flagged tile is re-run and rewritten by the exact instance later in
     // stream order, so its box may go out regardless
 #pragma unroll
@@ -922,7 +923,8 @@ __global__ void __launch_bounds__(NP * kSweepTL, PPMLR_SWEEP_MINB)
     atomicMin(A.err, s_err);
   }
   // the shared memory must outlive the stores' reads of it
-  if (threadIdx.x == 0 && store[0]) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  if (threadIdx.x == 0 && store[0] >= 0)
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 
 }  // namespace PPMLR_KNS

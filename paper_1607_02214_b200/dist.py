@@ -261,7 +261,7 @@ def _e2e_distributed(blk, ex, cfg, rank, world, args, cfl, srcs, cells_rank, loc
 
 
 def bench_distributed(args, METRIC, UNIT, ALG, make_config, ClockSampler, fp64_peak_tflops,
-                      measured_peaks, cpu_baseline):
+                      measured_peaks, cpu_baseline, workload):
     """bench.py's N-GPU arm: weak scaling, one 512^3 x-slab per rank."""
     import torch
     import torch.distributed as dist
@@ -315,9 +315,7 @@ def bench_distributed(args, METRIC, UNIT, ALG, make_config, ClockSampler, fp64_p
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "precision": args.precision, "data": "synthetic (deterministic IC, no RNG)",
-            "config": {"workload": cfg.name, "grid": [int(s.cells) for s in cfg.specs],
-                       "cells_per_gpu": cells_rank, "partition": f"x-slab ({world},1,1)",
-                       "l2": "state >> L2"},
+            "config": workload(args.config, world)[1],
             "clocks": clk.summary(), "gpu_launches": int(kernels),
             "halo": {"messages": ex.messages, "bytes": ex.bytes_moved},
             "roofline": {"bound": bound,
@@ -330,6 +328,8 @@ def bench_distributed(args, METRIC, UNIT, ALG, make_config, ClockSampler, fp64_p
                          "frac_hbm": fb, "frac_fp64": ff, "peak_hbm_source": hbm_src},
             "e2e": e2e,
         }
+        if not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(args.config)
         print(json.dumps(line), flush=True)
     blk.close()
     dist.destroy_process_group()

@@ -1,0 +1,134 @@
+"""BASELINE.json configurations at their stated sizes and step counts.
+
+* Strict build vs the REFERENCE: every case of tests/golden/baseline_runs.json
+  (written from the unmodified reference by make_golden_baseline.py) must be
+  reproduced bit for bit: each step's dt, the simulated time and the sha256
+  of the final interior.  C1 Brio-Wu 256x4x4 / 220 steps, C2 Orszag-Tang
+  512x512x4 / 100 steps, C3 magnetosphere 160x150x150 / 30 steps, plus blast
+  64^3 / 128^3 and a 64^3 dipole magnetosphere, grids on which every sweep
+  axis takes the compile-time tile (n % 64 == 0) the headline runs use.
+* Fast build vs strict (so vs the reference) on the same cases and on the
+  bench workloads themselves (C4 blast 512^3 for 25 steps, C5 1024x768x768
+  for 3 steps): per-field relative L1 <= 1e-11 and Linf <= 1e-9 (DESIGN.md
+  §2), compared on the device.
+
+The stepped function is Harness::advance (/root/reference/proj/src/
+harness.cpp:59-92)."""
+from __future__ import annotations
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, digest, rel_errors
+
+pytestmark = pytest.mark.gpu
+
+FAST_L1, FAST_LINF = 1e-11, 1e-9
+with open(os.path.join(GOLDEN, "baseline_runs.json")) as _f:
+    GOLD = json.load(_f)
+
+
+def _harness(gpu, rec, precision):
+    from paper_1607_02214_b200.api import AxisSpec, HarnessOptions
+    specs = [AxisSpec(*map(float, s[:5]), int(s[5]), float(s[6])) for s in rec["specs"]]
+    h = gpu.Harness(specs, (1, 1, 1), HarnessOptions(precision=precision, **rec["options"]))
+    if rec["ic"][0] == "mag":
+        h.init_magnetosphere()
+    else:
+        h.init_with(int(rec["ic"][0]), tuple(rec["ic"][1]))
+    return h
+
+
+@pytest.mark.parametrize("name", sorted(GOLD))
+def test_strict_reproduces_reference_digest(gpu, name):
+    rec = GOLD[name]
+    h = _harness(gpu, rec, "strict")
+    dts = [h.advance() for _ in range(rec["steps"])]
+    bad = [i for i, (a, b) in enumerate(zip(dts, rec["dts"])) if a.hex() != b]
+    assert not bad, f"dt differs from the reference first at step {bad[0]}"
+    assert h.time().hex() == rec["time"]
+    fin = h.gather_interior()
+    assert digest(fin) == rec["final_sha"], (
+        name, np.abs(fin).sum(axis=(0, 1, 2)).tolist(), rec["final_l1"])
+    h.close()
+
+
+@pytest.mark.parametrize("name", sorted(GOLD))
+def test_fast_within_tolerance_of_strict(gpu, name):
+    rec = GOLD[name]
+    out = {}
+    for prec in ("strict", "fast"):
+        h = _harness(gpu, rec, prec)
+        h.run(rec["steps"])
+        out[prec] = h.gather_interior()
+        h.close()
+    l1, linf = rel_errors(out["fast"], out["strict"])
+    print(name, "rel L1", l1.max(), "rel Linf", linf.max())
+    assert np.all(l1 <= FAST_L1) and np.all(linf <= FAST_LINF), (l1, linf)
+
+
+def _device_errors(a_fields, b_fields):
+    """Per-field relative L1 / Linf of a vs b, both lists of 8 device tensors."""
+    l1, linf = [], []
+    for a, b in zip(a_fields, b_fields):
+        d = (a - b).abs()
+        l1.append(float(d.sum() / b.abs().sum().clamp_min(1e-300)))
+        linf.append(float(d.max() / b.abs().max().clamp_min(1e-300)))
+    return np.array(l1), np.array(linf)
+
+
+@pytest.mark.slow
+def test_bench_workload_c4_blast512_fast_vs_strict(gpu):
+    """The headline workload itself: blast 512^3, 25 steps, both builds side
+    by side on the device (2 x 18 GB of state)."""
+    import torch
+    from paper_1607_02214_b200 import configs
+    hs = {}
+    for prec in ("strict", "fast"):
+        c = configs.blast(n=512, precision=prec)
+        hs[prec] = gpu.Harness(c.specs, c.partition, c.options)
+        configs.init(hs[prec], c)
+        hs[prec].run(25)
+    assert hs["strict"].time() != 0.0
+    rel_t = abs(hs["fast"].time() - hs["strict"].time()) / hs["strict"].time()
+    l1, linf = _device_errors(hs["fast"].block(0).state_view(), hs["strict"].block(0).state_view())
+    torch.cuda.synchronize()
+    print("blast512 rel L1", l1.max(), "rel Linf", linf.max(), "rel time", rel_t)
+    for h in hs.values():
+        h.close()
+    assert np.all(l1 <= FAST_L1) and np.all(linf <= FAST_LINF), (l1, linf)
+    assert rel_t <= 1e-12
+
+
+@pytest.mark.slow
+def test_bench_workload_c5_magnetosphere_fast_vs_strict(gpu):
+    """C5 1024x768x768 (dipole, stretched grid, frozen core) on one B200,
+    3 steps: the strict interior is kept on the device (38.6 GB) while the
+    fast harness runs, so the y/z dipole tiles of the headline C5 line are
+    checked at their real size."""
+    import torch
+    from paper_1607_02214_b200 import configs
+    c = configs.magnetosphere(nx=1024, nyz=768, d=0.05, precision="strict")
+    h = gpu.Harness(c.specs, c.partition, c.options)
+    configs.init(h, c)
+    h.run(3)
+    ref = [t.clone() for t in h.block(0).state_view()]
+    t_ref = h.time()
+    h.close()
+    del h
+    torch.cuda.empty_cache()
+    c = configs.magnetosphere(nx=1024, nyz=768, d=0.05, precision="fast")
+    h = gpu.Harness(c.specs, c.partition, c.options)
+    configs.init(h, c)
+    h.run(3)
+    l1, linf = _device_errors(h.block(0).state_view(), ref)
+    rel_t = abs(h.time() - t_ref) / t_ref
+    h.close()
+    del ref
+    torch.cuda.empty_cache()
+    print("mag1024 rel L1", l1.max(), "rel Linf", linf.max(), "rel time", rel_t)
+    assert np.all(l1 <= FAST_L1) and np.all(linf <= FAST_LINF), (l1, linf)
+    assert rel_t <= 1e-12
