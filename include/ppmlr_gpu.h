@@ -201,6 +201,9 @@ int ppmlr_gpu_block_synchronize(ppmlr_gpu_block* b);
  * ghost width (4).  For on-device consumers (analysis, comparisons). */
 int ppmlr_gpu_block_state_view(ppmlr_gpu_block* b, double** field_planes, long long* strides,
                                int* dims);
+/* The dipole field B_d (3 planes, same layout as the state) or NULLs;
+ * returns 1 when the block carries one. */
+int ppmlr_gpu_block_dipole_view(ppmlr_gpu_block* b, double** bd_planes);
 /* Error word check (host sync): returns the status of the first failure
  * recorded since the last check, with the reference's message. */
 int ppmlr_gpu_block_check(ppmlr_gpu_block* b);

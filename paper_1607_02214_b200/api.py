@@ -223,16 +223,22 @@ class Block:
     def synchronize(self):
         check(N.lib.ppmlr_gpu_block_synchronize(self.h))
 
-    def state_view(self, interior=True):
+    def state_view(self, interior=True, dipole=False):
         """The device-resident state as 8 torch tensors (z, y, x) viewing the
-        library's memory (no copy; valid until the next step or upload)."""
+        library's memory (no copy; valid until the next step or upload);
+        dipole=True: the 3 B_d planes instead (None without a dipole)."""
         import torch
         pl = (C.c_void_p * 8)()
         st = (C.c_longlong * 3)()
         dims = (C.c_int * 3)()
         g = N.lib.ppmlr_gpu_block_state_view(self.h, pl, st, dims)
+        if dipole:
+            bp = (C.c_void_p * 3)()
+            if not N.lib.ppmlr_gpu_block_dipole_view(self.h, bp):
+                return None
+            pl = list(bp) + [None] * 5
         out = []
-        for f in range(8):
+        for f in range(3 if dipole else 8):
             shape = (dims[2], dims[1], st[1])
             t = torch.as_tensor(_CudaArray(pl[f], shape, (st[2] * 8, st[1] * 8, 8)),
                                 device=f"cuda:{self.device}")

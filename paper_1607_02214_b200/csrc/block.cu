@@ -1105,6 +1105,158 @@ int block_upload_streamed(ppmlr_gpu_block* b, const ChunkFill& fill, bool with_b
 }
 
 // Pre-filled sunward shell, fresh error window and step counter.
+// ---------------------------------------------------------------- device setup
+// make_block's default state and dipole (stepper.cpp:63-69) and the built-in
+// init_with ICs (harness.cpp:35-43; kinds 0 uniform, 1 Brio-Wu, 2
+// Orszag-Tang, 3 blast) evaluated on the device, straight into the SoA
+// buffers.  The expressions are the host restatement's (host.cpp make_ic /
+// dipole) in the same IEEE operation order; this TU is compiled with
+// --fmad=false and IEEE `/` and `sqrt`, so every value is bit-identical to
+// the host path.  The one transcendental, Orszag-Tang's sin(), depends on a
+// single coordinate: the host evaluates it per x / y centre (std::sin, as
+// the reference) and the kernel reads those tables.
+struct InitArgs {
+  const double* cen[3];  // kG-ghost centre windows (S[a] entries)
+  const double* tab;     // kind 2: sin(x_i) [S0], sin(2 x_i) [S0], sin(y_j) [S1]
+  double p[8];
+  int kind;
+  double mu0;
+};
+
+__device__ __forceinline__ double dot3d(double ax, double ay, double az, double bx, double by,
+                                        double bz) {
+  return (ax * bx + ay * by) + az * bz;
+}
+
+__global__ void init_state_kernel(Planes d0, Planes d1, double* bd0, double* bd1, double* bd2,
+                                  Lay L, int S0, int S1, int S2, InitArgs A, int* err) {
+  const long long total = (long long)S0 * S1 * S2;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int il = (int)(t % S0), jl = (int)((t / S0) % S1), kl = (int)(t / ((long long)S0 * S1));
+    const double x = A.cen[0][il], y = A.cen[1][jl], z = A.cen[2][kl];
+    double s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    switch (A.kind) {
+      case -2:  // make_block: {1, 0, 0, 1}
+        s[0] = 1.0;
+        s[7] = 1.0;
+        break;
+      case 0:
+        for (int f = 0; f < 8; ++f) s[f] = A.p[f];
+        break;
+      case 1: {  // Brio-Wu
+        const bool left = x < 0.5;
+        s[0] = left ? 1.0 : 0.125;
+        s[7] = left ? 1.0 : 0.1;
+        s[4] = 0.75;
+        s[5] = left ? 1.0 : -1.0;
+        s[6] = 0.0;
+        break;
+      }
+      case 2: {  // Orszag-Tang
+        const double g = A.p[0];
+        const double sx = A.tab[il], s2x = A.tab[S0 + il], sy = A.tab[2 * S0 + jl];
+        s[0] = g * g;
+        s[7] = g;
+        s[1] = -sy;
+        s[2] = sx;
+        s[3] = 0.0;
+        s[4] = -sy;
+        s[5] = s2x;
+        s[6] = 0.0;
+        break;
+      }
+      case 3: {  // blast per unit block
+        const double cx = floor(x + 0.5);
+        const double dx = x - cx;
+        const double r2 = (dx * dx + y * y) + z * z;
+        s[0] = 1.0;
+        s[7] = r2 < A.p[2] * A.p[2] ? A.p[0] : A.p[1];
+        s[4] = sqrt(0.5);
+        s[5] = sqrt(0.5);
+        break;
+      }
+    }
+    const long long d = L.idx(il - kG, jl - kG, kl - kG);
+#pragma unroll
+    for (int f = 0; f < 8; ++f) {
+      d0.f[f][d] = s[f];
+      d1.f[f][d] = s[f];
+    }
+    if (bd0) {  // physics.cpp:14-21 dipole_field, moment (0, 0, -4 pi)
+      const double kPiD = 3.14159265358979323846;
+      const double mx = 0.0, my = 0.0, mz = -4.0 * kPiD;
+      const double r2 = dot3d(x, y, z, x, y, z);
+      if (r2 == 0.0) {
+        atomicOr(err, 1);
+        continue;
+      }
+      const double r = sqrt(r2);
+      const double rx = x / r, ry = y / r, rz = z / r;
+      const double k = A.mu0 / (4.0 * kPiD);
+      const double sm = 3.0 * dot3d(mx, my, mz, rx, ry, rz);
+      const double vx = rx * sm - mx, vy = ry * sm - my, vz = rz * sm - mz;
+      const double den = r2 * r;
+      bd0[d] = (vx * k) / den;
+      bd1[d] = (vy * k) / den;
+      bd2[d] = (vz * k) / den;
+    }
+  }
+}
+
+bool device_init_supported(int kind) { return kind >= -2 && kind <= 3 && kind != -1; }
+
+int block_init_device(ppmlr_gpu_block* b, int kind, const double* params, bool with_bd) {
+  CK(cudaSetDevice(b->device));
+  CK(cudaStreamSynchronize(b->stream));
+  with_bd = with_bd && b->with_dipole && b->bd;
+  InitArgs A{};
+  A.kind = kind;
+  A.mu0 = b->c.mu0;
+  if (params)
+    for (int f = 0; f < 8; ++f) A.p[f] = params[f];
+  std::vector<double> tab;
+  size_t ncen = 0;
+  for (int a = 0; a < 3; ++a) ncen += b->S[a];
+  if (kind == 2) {
+    tab.resize(2 * (size_t)b->S[0] + b->S[1]);
+    for (int i = 0; i < b->S[0]; ++i) {
+      tab[i] = std::sin(b->h_centers[0][i]);
+      tab[b->S[0] + i] = std::sin(2.0 * b->h_centers[0][i]);
+    }
+    for (int j = 0; j < b->S[1]; ++j) tab[2 * b->S[0] + j] = std::sin(b->h_centers[1][j]);
+  }
+  const size_t need = sizeof(double) * (ncen + tab.size()) + sizeof(int);
+  if (int rc = ensure_scratch(b, need)) return rc;
+  std::vector<double> host(ncen + tab.size());
+  size_t off = 0;
+  for (int a = 0; a < 3; ++a) {
+    std::copy(b->h_centers[a].begin(), b->h_centers[a].end(), host.begin() + off);
+    A.cen[a] = b->d_scratch + off;
+    off += b->S[a];
+  }
+  std::copy(tab.begin(), tab.end(), host.begin() + off);
+  A.tab = b->d_scratch + off;
+  int* d_err = reinterpret_cast<int*>(b->d_scratch + host.size());
+  CK(cudaMemcpyAsync(b->d_scratch, host.data(), sizeof(double) * host.size(),
+                     cudaMemcpyHostToDevice, b->stream));
+  CK(cudaMemsetAsync(d_err, 0, sizeof(int), b->stream));
+  const long long total = (long long)b->S[0] * b->S[1] * b->S[2];
+  init_state_kernel<<<grid_for(total), 256, 0, b->stream>>>(
+      planes(b->buf[0], b->ncell), planes(b->buf[1], b->ncell), with_bd ? b->bd : nullptr,
+      with_bd ? b->bd + b->ncell : nullptr, with_bd ? b->bd + 2 * b->ncell : nullptr, lay_of(b),
+      b->S[0], b->S[1], b->S[2], A, d_err);
+  CK(cudaGetLastError());
+  int herr = 0;
+  CK(cudaMemcpyAsync(&herr, d_err, sizeof(int), cudaMemcpyDeviceToHost, b->stream));
+  CK(cudaStreamSynchronize(b->stream));
+  if (herr) {
+    set_error("dipole_field evaluated at the singularity");
+    return PPMLR_UNPHYSICAL;
+  }
+  return block_finish_upload(b);
+}
+
 int block_finish_upload(ppmlr_gpu_block* b) {
   b->dt_valid = false;  // state or dt slot changes
   const Lay L = lay_of(b);
@@ -1560,6 +1712,11 @@ int ppmlr_gpu_block_state_view(ppmlr_gpu_block* b, double** field_planes, long l
   strides[2] = b->sz;
   for (int a = 0; a < 3; ++a) dims[a] = b->S[a];
   return kG;
+}
+
+int ppmlr_gpu_block_dipole_view(ppmlr_gpu_block* b, double** bd_planes) {
+  for (int a = 0; a < 3; ++a) bd_planes[a] = b->bd ? b->bd + (long long)a * b->ncell : nullptr;
+  return b->bd ? 1 : 0;
 }
 
 int ppmlr_gpu_block_timing(ppmlr_gpu_block* b, int enable, double* sweep_ms, double* total_ms,

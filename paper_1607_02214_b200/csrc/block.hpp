@@ -153,4 +153,8 @@ int block_set_frozen(ppmlr_gpu_block* b, const int64_t* frozen_idx, const double
 int block_upload_streamed(ppmlr_gpu_block* b, const ChunkFill& fill, bool with_bd,
                           const double* src_fields = nullptr, const double* src_bd = nullptr);
 int block_finish_upload(ppmlr_gpu_block* b);
+// Device-side setup (make_block default + dipole, init_with kinds 0..3),
+// bit-identical to the host path; frozen set untouched.
+bool device_init_supported(int kind);
+int block_init_device(ppmlr_gpu_block* b, int kind, const double* params, bool with_bd);
 }  // namespace ppmlr_b200

@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <stdexcept>
@@ -602,6 +603,25 @@ void upload_init(ppmlr_gpu_harness* h, int r, ChunkInit ci, bool with_bd) {
     throw SpecError(e, ppmlr_gpu_last_error());
 }
 
+// Device-side setup (block.cu block_init_device) for make_block's default
+// state + dipole and init_with kinds 0..3; bit-identical to upload_init's
+// host evaluation (tests/test_gpu_setup.py).  PPMLR_HOST_INIT=1 forces the
+// host path.
+bool use_device_init(int kind) {
+  const char* e = std::getenv("PPMLR_HOST_INIT");
+  return device_init_supported(kind) && !(e && std::atoi(e) != 0);
+}
+
+void init_device(ppmlr_gpu_harness* h, int r, int kind, const double* params, bool with_bd) {
+  h->fidx[r].clear();
+  h->fst[r].clear();
+  ppmlr_gpu_block* b = h->blocks[r];
+  if (int e = block_set_frozen(b, nullptr, nullptr, 0)) throw SpecError(e, ppmlr_gpu_last_error());
+  double p[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (params) std::memcpy(p, params, sizeof p);
+  if (int e = block_init_device(b, kind, p, with_bd)) throw SpecError(e, ppmlr_gpu_last_error());
+}
+
 // Ledger entry of one exchange_step (exchange.cpp:93-149): every interior
 // face both ways, payload face_cells*ghost*8 doubles; staged adds 6 copies.
 void record_exchange(ppmlr_gpu_harness* h, long step) {
@@ -814,9 +834,13 @@ int ppmlr_gpu_harness_create(const ppmlr_axis_spec specs[3], int px, int py, int
           throw SpecError(e, ppmlr_gpu_last_error());
       }
       // make_block's default state {1, 0, 0, 1} and its dipole
-      ChunkInit ci;
-      ci.kind = -2;
-      upload_init(h, (int)r, ci, true);
+      if (use_device_init(-2)) {
+        init_device(h, (int)r, -2, nullptr, true);
+      } else {
+        ChunkInit ci;
+        ci.kind = -2;
+        upload_init(h, (int)r, ci, true);
+      }
     }
     return 0;
   });
@@ -852,6 +876,10 @@ int ppmlr_gpu_harness_init_magnetosphere(ppmlr_gpu_harness* h, double rho_core, 
 int ppmlr_gpu_harness_init_ic(ppmlr_gpu_harness* h, int kind, const double* params) {
   return guarded([&] {
     for (size_t r = 0; r < h->blocks.size(); ++r) {
+      if (use_device_init(kind)) {
+        init_device(h, (int)r, kind, params, false);
+        continue;
+      }
       ChunkInit ci;
       ci.kind = kind;
       ci.ic = ic_of(kind, params);
