@@ -2,5 +2,8 @@
 // gated by the tolerance in DESIGN.md / tests/test_gpu_parity.py.
 #define PPMLR_FAST_MATH 1
 #define PPMLR_KNS fast
+#ifndef PPMLR_SWEEP_V2_ON
+#define PPMLR_SWEEP_V2_ON 1  // sweep_v2.cuh schedule for the no-dipole compile-time tile
+#endif
 #define PPMLR_LAUNCH_NAME launch_sweep_fast
 #include "sweep_launch.inc"

@@ -1,0 +1,428 @@
+// Persistent, prefetching schedule of the directional PPMLR sweep (fast
+// build, no dipole): the same per-pencil algorithm as sweep.cuh's
+// sweep_tile (proj/src/ppm1d.cpp:111-364, stepper.cpp:249-282) with three
+// changes of schedule, measured against the one-shot kernel on the B200:
+//
+//  * Persistent CTAs (3 per SM) walk the tiles; the tile's 8 input planes
+//    arrive by TMA in one of two FLD buffers, and the elected thread issues
+//    the NEXT tile's loads when the current tile starts, so the HBM latency
+//    of a tile load is hidden behind a whole tile of compute (the one-shot
+//    kernel waited for it: ~12% of the sweep's stall samples).
+//  * The conserved state is not stored by P0: P7 recomputes it from the
+//    zone's own primitives (prim_to_cons, the same expressions), and only
+//    tiles with a moving edge write it (into the dead FLD slots) for the
+//    remap parabolas.  That frees the 8 slots the prefetch buffer needs:
+//    2 x 8 (FLD) + 8 (TR) + 8 (LFT) + 1 (CF) = 33 slots, as before.
+//  * The Lagrangian Riemann problem at edge s+1 is solved by the thread of
+//    zone s, which still holds that zone's traced RIGHT state in registers:
+//    the right states never go through shared memory and the write-after-
+//    read barrier in the middle of P3 disappears.
+//
+// Phases and barriers of one tile (non-moving tiles skip P7b/P8):
+//   [TMA wait] P0 | P3 | P4 (+moving vote) | P7 | P7b | P8 | slivers | P9 | close
+//   P0   strip-frame prim -> cf (CF), primitive slopes (TR)
+//   P3   traced states: left -> LFT, right kept in registers
+//   P4   edge s+1: u* -> CF[s+1], flux -> TR[s+1]
+//   P7   Lagrangian update -> lag (LFT); moving tiles: cons -> FLD
+//   P7b  moving: conserved slopes -> TR
+//   P8   moving: slivers (registers), then -> TR
+//   P9   remap + cons_to_prim -> FLD (TMA box store) or global
+#pragma once
+#include "sweep.cuh"
+
+namespace ppmlr_b200 {
+namespace PPMLR_KNS {
+
+template <int AXIS, int NP, int TL, class Ops>
+__device__ __forceinline__ bool sweep_tile_v2(const SweepArgs& A, const SweepMaps& M,
+                                              const TileId id, double* smem, double* FLD,
+                                              unsigned long long* s_err, bool& stored) {
+  bool tbad = false;
+  constexpr int NT = NP * TL;
+  constexpr int T = slot_stride(NT);
+  double* TR = smem + 16 * T;
+  double* LFT = smem + 24 * T;
+  double* CF = smem + 32 * T;
+  constexpr int SS = AXIS == 0 ? 1 : NP;
+  const int seg = id.seg, grp = id.grp, oc = id.oc;
+  const int nn = A.n + 8;
+  const int seg0 = seg * A.L;
+  const int TLv = min(TL, nn - seg0);
+  const bool final_seg = seg == A.nseg - 1;
+  const int zmax = final_seg ? TLv - 2 : TL - 3;
+  const int g0 = grp * NP;
+  const int npv = min(NP, A.ng - g0);
+  const bool whole = TLv == TL && npv == NP;
+  const double dt = *A.dt;
+  const Consts& c = A.c;
+  const KC k = make_kc(c);
+  const int ci = threadIdx.x;
+  int s, p;
+  if (AXIS == 0) {
+    p = ci / TL;
+    s = ci - p * TL;
+  } else {
+    s = ci / NP;
+    p = ci - s * NP;
+  }
+  const bool live = ci < NT && p < npv;
+  const int q = seg0 + s;
+  auto pencil_index = [&]() -> unsigned long long {
+    const int gcoord = g0 + p;
+    const int t1 = AXIS == 1 ? oc : gcoord;
+    const int t2 = AXIS == 1 ? gcoord : oc;
+    return (unsigned long long)t1 + (unsigned long long)A.nb * (unsigned long long)t2;
+  };
+  constexpr int a = AXIS, b = (AXIS + 1) % 3, d = (AXIS + 2) % 3;
+  constexpr int fof[8] = {0, 1 + a, 1 + b, 1 + d, 4 + a, 4 + b, 4 + d, 7};
+
+  // ---- P0: cf and primitive slopes ----------------------------------------
+  if (live && s < TLv) {
+    double qv[8];
+#pragma unroll
+    for (int f = 0; f < 8; ++f) qv[f] = FLD[f * T + ci];
+    Ops o;
+    CF[ci] = fast_speed3<AXIS>(qv, 0.0, 0.0, 0.0, k, o);
+    tbad |= o.bad;
+    if (s >= 1 && s <= TLv - 2) {
+      const double* gc = A.slope + 3 * q;
+      const double c0 = __ldg(gc), cA = __ldg(gc + 1), cB = __ldg(gc + 2);
+#pragma unroll
+      for (int v = 0; v < 8; ++v) {
+        const double* pv = FLD + fof[v] * T + ci;
+        TR[v * T + ci] = limited_slope(pv[-SS], pv[0], pv[SS], c0, cA, cB);
+      }
+    }
+  }
+  __syncthreads();
+
+  // ---- P3: traced states of zones [2, zmax]; L -> LFT, R in registers ------
+  double R[8];
+  const bool z3 = live && s >= 2 && s <= zmax;
+  if (z3) {
+    const bool flat = q >= nn - 2;
+    double e0[5], e1[5];
+#pragma unroll
+    for (int j = 0; j < 5; ++j) {
+      e0[j] = __ldg(A.qfc + 5 * q + j);
+      e1[j] = __ldg(A.qfc + 5 * (q + 1) + j);
+    }
+    Ops o;
+    const double sigma =
+        sclamp(o.div(CF[ci] * dt, __ldg(A.dx + q), __ldg(A.rdx + q)), 0.0, 1.0);
+    const double hs = 0.5 * sigma;
+    const double tw = tw_of(sigma, k, o);
+    auto trace = [&](auto F, const int v, double& l, double& r) {
+      const double* pv = FLD + fof[v] * T + ci;
+      const double av = pv[0];
+      double al = av, ar = av, six = 0.0;
+      if (!decltype(F)::value) {
+        const double* dv = TR + v * T + ci;
+        auto win = [&](int j) { return pv[j * SS]; };
+        auto dwin = [&](int j) { return dv[j * SS]; };
+        zone_parabola_dm(win, dwin, e0, e1, k, o, al, ar, six);
+      }
+      l = avg_left(al, ar, six, hs, tw);
+      r = avg_right(al, ar, six, hs, tw);
+    };
+    auto all8 = [&](auto F) {
+      double Lr, Lp;
+      trace(F, kRho, Lr, R[kRho]);
+      trace(F, kPE, Lp, R[kPE]);
+      const bool badL = !(Lr > 0.0) || !(Lp > 0.0);
+      const bool badR = !(R[kRho] > 0.0) || !(R[kPE] > 0.0);
+#pragma unroll
+      for (int v = 0; v < 8; ++v) {
+        double l = v == kRho ? Lr : Lp;
+        if (v != kRho && v != kPE) trace(F, v, l, R[v]);
+        LFT[v * T + ci] = l;
+      }
+      if (badL || badR) {  // rare: the zone falls back to its own state
+#pragma unroll
+        for (int v = 0; v < 8; ++v) {
+          const double own = FLD[fof[v] * T + ci];
+          if (badL) LFT[v * T + ci] = own;
+          if (badR) R[v] = own;
+        }
+      }
+    };
+    if (flat)
+      all8(FlatTag<true>{});
+    else
+      all8(FlatTag<false>{});
+    tbad |= o.bad;
+  }
+  __syncthreads();
+
+  // ---- P4: edge m = s + 1 in [3, zmax] by the thread of zone s ------------
+  bool mv = false;
+  if (live && s >= 2 && s <= zmax - 1) {
+    double f[8];
+    const double bz[3] = {0.0, 0.0, 0.0};
+    const SmemVec qr{LFT + ci + SS, T};
+    Ops o;
+    const double us = solve_edge(R, qr, bz, bz, k, f, o);
+    tbad |= o.bad;
+    CF[ci + SS] = us;
+    mv = s + 1 >= 4 && s + 1 <= TLv - 4 && us * dt != 0.0;
+#pragma unroll
+    for (int v = 0; v < 8; ++v) TR[v * T + ci + SS] = f[v];
+  }
+  const bool moving = __syncthreads_or(mv);
+
+  // ---- P7: Lagrangian update of zones [3, zmax-1] -> LFT -------------------
+  // (moving tiles: every cell's conserved state -> FLD for the remap)
+  if (live && s < TLv && (moving || (s >= 3 && s <= zmax - 1))) {
+    double w[8];
+#pragma unroll
+    for (int v = 0; v < 8; ++v) w[v] = FLD[fof[v] * T + ci];
+    Ops o;
+    double cons[8];
+    cons[kRho] = w[kRho];
+    cons[kUn] = w[kRho] * w[kUn];
+    cons[kUt1] = w[kRho] * w[kUt1];
+    cons[kUt2] = w[kRho] * w[kUt2];
+    cons[kBn] = w[kBn];
+    cons[kBt1] = w[kBt1];
+    cons[kBt2] = w[kBt2];
+    cons[kPE] = strip_energy(w, k, o);
+    if (s >= 3 && s <= zmax - 1) {
+      const double dx0 = __ldg(A.dx + q);
+      const double dxp = dx0 + dt * (CF[ci + SS] - CF[ci]);
+      if (!(dxp > 0.0)) {
+        atomicMin(s_err, err_key(*A.step, A.phase, AXIS,
+                                 (pencil_index() << 20) | ((unsigned long long)q << 2) |
+                                     kErrStepRejected));
+      } else {
+        double u[8];
+        const double r_dxp = o.rcp(dxp);
+        const double shrink = o.div(dx0, dxp, r_dxp);
+#pragma unroll
+        for (int v = 0; v < 8; ++v)
+          u[v] = cons[v] * shrink -
+                 o.div(dt * (TR[v * T + ci + SS] - TR[v * T + ci]), dxp, r_dxp);
+        const double internal =
+            (u[kPE] - o.dv(0.5 * ((u[kUn] * u[kUn] + u[kUt1] * u[kUt1]) + u[kUt2] * u[kUt2]),
+                           u[kRho])) -
+            o.div((u[kBn] * u[kBn] + u[kBt1] * u[kBt1]) + u[kBt2] * u[kBt2], c.two_mu0,
+                  k.r_two_mu0);
+#pragma unroll
+        for (int v = 0; v < 8; ++v) LFT[v * T + ci] = u[v];
+        if (c.pressure_floor <= 0.0 && (!(u[kRho] > 0.0) || !(internal > 0.0)))
+          atomicMin(s_err, err_key(*A.step, A.phase, AXIS,
+                                   (pencil_index() << 20) | ((unsigned long long)q << 2) |
+                                       kErrLagUnphysical));
+      }
+    }
+    tbad |= o.bad;
+    if (moving) {
+#pragma unroll
+      for (int v = 0; v < 8; ++v) FLD[v * T + ci] = cons[v];
+    }
+  }
+  __syncthreads();
+
+  const bool e8 = live && s >= 4 && s <= TLv - 4;
+  if (moving) {
+    // ---- P7b: conserved slopes at [1, TLv-2] -> TR (fluxes dead) ----------
+    if (live && s >= 1 && s <= TLv - 2) {
+      const double* gc = A.slope + 3 * q;
+      const double c0 = __ldg(gc), cA = __ldg(gc + 1), cB = __ldg(gc + 2);
+#pragma unroll
+      for (int v = 0; v < 8; ++v) {
+        const double* cv = FLD + v * T + ci;
+        TR[v * T + ci] = limited_slope(cv[-SS], cv[0], cv[SS], c0, cA, cB);
+      }
+    }
+    __syncthreads();
+    // ---- P8: slivers at edges [4, TLv-4] --------------------------------
+    double sl[8];
+#pragma unroll
+    for (int v = 0; v < 8; ++v) sl[v] = 0.0;
+    if (e8) {
+      const double delta = CF[ci] * dt;
+      if (delta != 0.0) {
+        const bool right = delta > 0.0;
+        const int kc = right ? ci - SS : ci;  // upwind zone
+        const int kq = right ? q - 1 : q;
+        const double width = __ldg(A.dx + kq) + dt * (CF[kc + SS] - CF[kc]);
+        double e0[5], e1[5];
+#pragma unroll
+        for (int j = 0; j < 5; ++j) {
+          e0[j] = __ldg(A.qfc + 5 * kq + j);
+          e1[j] = __ldg(A.qfc + 5 * (kq + 1) + j);
+        }
+        Ops o;
+        const double sigma = o.dv(right ? delta : -delta, width);
+        const double hs = 0.5 * sigma;
+        const double tw = tw_of(sigma, k, o);
+#pragma unroll
+        for (int v = 0; v < 8; ++v) {
+          const double* cv = FLD + v * T + kc;
+          const double* dv = TR + v * T + kc;
+          auto win = [&](int j) { return cv[j * SS]; };
+          auto dwin = [&](int j) { return dv[j * SS]; };
+          double al, ar, six;
+          zone_parabola_dm(win, dwin, e0, e1, k, o, al, ar, six);
+          const double mean =
+              right ? avg_right(al, ar, six, hs, tw) : avg_left(al, ar, six, hs, tw);
+          sl[v] = delta * (mean + (LFT[v * T + kc] - cv[0]));
+        }
+        tbad |= o.bad;
+      }
+    }
+    __syncthreads();
+    if (e8) {
+#pragma unroll
+      for (int v = 0; v < 8; ++v) TR[v * T + ci] = sl[v];
+    }
+    __syncthreads();
+  }
+
+  // ---- P9: remap, cons_to_prim, store (zones [4, TLv-5]) ------------------
+  stored = whole && PPMLR_SWEEP_TMA_STORE;
+  if (live && s >= 4 && s <= TLv - 5) {
+    const double dxe = __ldg(A.dx + q);
+    const double r_dxe = __ldg(A.rdx + q);
+    const double width = dxe + dt * (CF[ci + SS] - CF[ci]);
+    double out[8], u[8], cs[8];
+    Ops o;
+    const double scale = o.div(width, dxe, r_dxe);
+    if (moving) {
+#pragma unroll
+      for (int v = 0; v < 8; ++v)
+        u[v] = LFT[v * T + ci] * scale + o.div(TR[v * T + ci] - TR[v * T + ci + SS], dxe, r_dxe);
+    } else {
+#pragma unroll
+      for (int v = 0; v < 8; ++v) u[v] = LFT[v * T + ci] * scale;
+    }
+    cs[0] = u[kRho];
+    cs[1 + a] = u[kUn];
+    cs[1 + b] = u[kUt1];
+    cs[1 + d] = u[kUt2];
+    cs[4 + a] = u[kBn];
+    cs[4 + b] = u[kBt1];
+    cs[4 + d] = u[kBt2];
+    cs[7] = u[kPE];
+    const int bad = cons_to_prim3(cs, out, k, o);
+    tbad |= o.bad;
+    if (bad) {
+      atomicMin(s_err, err_key(*A.step, A.phase, AXIS,
+                               (pencil_index() << 20) | (1ull << 19) |
+                                   ((unsigned long long)(q - 4) << 2) |
+                                   (bad == 1 ? kErrDensity : kErrPressure)));
+    } else if (stored) {
+      // dense box order of the L interior zones x NP pencils (FLD is dead)
+      const int bi = AXIS == 0 ? p * A.L + (s - 4) : (s - 4) * NP + p;
+#pragma unroll
+      for (int f = 0; f < 8; ++f) FLD[f * T + bi] = out[f];
+    } else {
+      const long long off = (long long)(g0 + p + 4) * A.stride_g +
+                            (long long)(oc + 4) * A.stride_o + (long long)q * A.stride_a;
+#pragma unroll
+      for (int f = 0; f < 8; ++f) A.dst[f][off] = out[f];
+    }
+  }
+  if (stored) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  return tbad;
+}
+
+// One elected thread: the 8 field boxes of tile `id` into FLD, on `mbar`.
+template <int AXIS, int NP, int TL>
+__device__ __forceinline__ void tma_load_fields(const SweepArgs& A, const SweepMaps& M,
+                                                const TileId id, double* FLD,
+                                                unsigned long long* mbar) {
+  constexpr int T = slot_stride(NP * TL);
+  constexpr unsigned kBox = NP * TL * sizeof(double);
+  const int a0 = id.seg * A.L, g = id.grp * NP + 4, o = id.oc + 4;
+  const int cx = AXIS == 0 ? a0 : g;
+  const int cy = AXIS == 0 ? g : (AXIS == 1 ? a0 : o);
+  const int cz = AXIS == 2 ? a0 : o;
+  const unsigned bar = smem_u32(mbar);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+               "r"(kBox * 8u)
+               : "memory");
+#pragma unroll
+  for (int f = 0; f < 8; ++f)
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(FLD + f * T)),
+        "l"(reinterpret_cast<unsigned long long>(&M.f[f])), "r"(cx), "r"(cy), "r"(cz),
+        "r"(bar)
+        : "memory");
+}
+
+__device__ __forceinline__ TileId tile_of_v2(int t, int nseg, int ngroups) {
+  const int rest = t / nseg;
+  return {t - rest * nseg, rest % ngroups, rest / ngroups};
+}
+
+// Persistent main instance (grid = min(tiles, resident CTAs)); flagged
+// tiles go to the EXACT instance of sweep.cuh as before.
+template <int AXIS, int NP, int TL>
+__global__ void __launch_bounds__(NP * TL, 3)
+    sweep_kernel_v2(const SweepArgs A, const __grid_constant__ SweepMaps M) {
+  extern __shared__ __align__(128) double smem[];
+  __shared__ unsigned long long s_err;
+  __shared__ __align__(8) unsigned long long s_mbar[2];
+  constexpr int T = slot_stride(NP * TL);
+  const int ntiles = A.nseg * A.ngroups * A.no;
+  int t = blockIdx.x;
+  if (threadIdx.x == 0) {
+    s_err = kNoError;
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&s_mbar[0])) : "memory");
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&s_mbar[1])) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (t < ntiles)
+      tma_load_fields<AXIS, NP, TL>(A, M, tile_of_v2(t, A.nseg, A.ngroups), smem, &s_mbar[0]);
+  }
+  __syncthreads();
+#pragma unroll 1
+  for (int i = 0; t < ntiles; ++i, t += gridDim.x) {
+    const int buf = i & 1;
+    double* FLD = smem + buf * 8 * T;
+    const TileId id = tile_of_v2(t, A.nseg, A.ngroups);
+    if (threadIdx.x == 0) {
+      const int tn = t + gridDim.x;
+      if (tn < ntiles) {
+        // the other buffer held the previous tile's result box: its TMA
+        // store must have read it before the next tile's fields land there
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        tma_load_fields<AXIS, NP, TL>(A, M, tile_of_v2(tn, A.nseg, A.ngroups),
+                                      smem + (buf ^ 1) * 8 * T, &s_mbar[buf ^ 1]);
+      }
+    }
+    mbar_wait(&s_mbar[buf], (unsigned)(i >> 1) & 1u);
+    bool stored = false;
+    const bool bad = sweep_tile_v2<AXIS, NP, TL, MainOps>(A, M, id, smem, FLD, &s_err, stored);
+    const bool any_bad = __syncthreads_or(bad);
+    if (threadIdx.x == 0) {
+      if (stored) {
+        const int a0 = id.seg * A.L + 4, g = id.grp * NP + 4, o = id.oc + 4;
+        const int c0 = AXIS == 0 ? a0 : g;
+        const int c1 = AXIS == 0 ? g : (AXIS == 1 ? a0 : o);
+        const int c2 = AXIS == 2 ? a0 : o;
+#pragma unroll
+        for (int f = 0; f < 8; ++f)
+          asm volatile(
+              "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                  reinterpret_cast<unsigned long long>(&M.out[f])),
+              "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(FLD + f * T))
+              : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+      if (any_bad)
+        A.redo_list[atomicAdd(A.redo_count, 1u)] = t;
+      else if (s_err != kNoError)
+        atomicMin(A.err, s_err);
+      s_err = kNoError;
+    }
+  }
+  // the shared memory must outlive the last stores' reads of it
+  if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+
+}  // namespace PPMLR_KNS
+}  // namespace ppmlr_b200

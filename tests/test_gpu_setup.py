@@ -40,7 +40,7 @@ def _cases():
     tp = 2.0 * math.pi
     yield "default+dipole C3", configs.magnetosphere().specs, HarnessOptions(
         boundary=2, with_dipole=True), None
-    yield "default+dipole C5-shaped", configs.magnetosphere(nx=128, nyz=96, d=0.4).specs, \
+    yield "default+dipole C5-shaped", configs.magnetosphere(nx=256, nyz=192, d=0.2).specs, \
         HarnessOptions(boundary=2, with_dipole=True), None
     cube = [AxisSpec.uniform(-0.5, 0.5, 24)] * 3
     yield "blast", [AxisSpec(-0.5, 1.5, -0.5, 1.5, 1 / 20, 40, 1.05)] + cube[1:], \
@@ -51,8 +51,8 @@ def _cases():
     yield "uniform", cube, HarnessOptions(), (0, (1.0, 0.1, -0.2, 0.3, 0.5, 0.6, 0.7, 2.0))
     yield "blast ghost 6", cube, HarnessOptions(ghost=6), (3, (10.0, 0.1, 0.2))
     yield "dipole stretched odd", [AxisSpec(-100.0, 30.0, -10.0, 10.0, 2.5, 41, 1.05),
-                                   AxisSpec(-100.0, 100.0, -10.0, 10.0, 2.5, 37, 1.05),
-                                   AxisSpec(-100.0, 100.0, -10.0, 10.0, 2.5, 33, 1.05)], \
+                                   AxisSpec(-100.0, 100.0, -10.0, 10.0, 2.5, 40, 1.05),
+                                   AxisSpec(-100.0, 100.0, -10.0, 10.0, 2.0, 48, 1.05)], \
         HarnessOptions(boundary=2, with_dipole=True), (3, (2.0, 1.0, 0.3))
     del tp
 
@@ -73,7 +73,7 @@ def test_device_setup_matches_host_block_state(gpu):
     """The device-initialised state equals host_block_state (the host
     restatement used by the CPU tests) on the kG window."""
     from paper_1607_02214_b200 import configs
-    c = configs.magnetosphere(nx=64, nyz=48, d=1.0)
+    c = configs.magnetosphere()
     h = gpu.Harness(c.specs, (1, 1, 1), c.options)
     h.init_with(3, (5.0, 0.5, 10.0))
     st = gpu.host_block_state(c.specs, (1, 1, 1), c.options, 0, (3, (5.0, 0.5, 10.0)))
