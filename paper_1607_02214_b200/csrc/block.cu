@@ -519,6 +519,7 @@ int launch_sweep(ppmlr_gpu_block* b, int axis, int phase) {
   A.c = b->c;
   A.redo_count = b->d_redo;
   A.redo_list = b->d_redo + 1;
+  A.tile_ctr = b->d_redo + b->redo_cap + 1;
   const int T = slot_stride(kSweepNP * (A.L + 8));
   // shared slots per cell: 25 (+3 dipole), 33 with the extra-slot schedule
   // (sweep.cuh XS; with the dipole only in the strict build)
@@ -897,7 +898,7 @@ int ppmlr_gpu_block_create(const ppmlr_gpu_block_desc* d, ppmlr_gpu_block** out)
     }
     const long long cells = (long long)b->n[0] * b->n[1] * b->n[2];
     b->redo_cap = (unsigned)std::max<long long>(tiles, std::min<long long>(cells, 1 << 22));
-    if ((e = cudaMalloc(&b->d_redo, sizeof(unsigned) * ((size_t)b->redo_cap + 1))) != cudaSuccess)
+    if ((e = cudaMalloc(&b->d_redo, sizeof(unsigned) * ((size_t)b->redo_cap + 2))) != cudaSuccess)
       return fail(cuda_fail(e, "cudaMalloc(redo)"));
   }
   *out = b;

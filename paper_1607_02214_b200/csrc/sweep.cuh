@@ -146,6 +146,7 @@ struct SweepArgs {
   Consts c;
   unsigned* redo_count;  // tiles whose fast-path guards failed ...
   unsigned* redo_list;   // ... are re-run exactly by the EXACT instance
+  unsigned* tile_ctr;    // persistent schedule (sweep_v2.cuh): tiles claimed so far
 };
 
 namespace PPMLR_KNS {

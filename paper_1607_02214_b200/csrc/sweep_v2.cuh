@@ -357,34 +357,50 @@ __device__ __forceinline__ TileId tile_of_v2(int t, int nseg, int ngroups) {
   return {t - rest * nseg, rest % ngroups, rest / ngroups};
 }
 
+#ifndef PPMLR_SWEEP_V2_MINB
+#define PPMLR_SWEEP_V2_MINB 3
+#endif
+#ifndef PPMLR_SWEEP_V2_DYN
+#define PPMLR_SWEEP_V2_DYN 1  // tiles beyond the first wave claimed from a counter
+#endif
+
 // Persistent main instance (grid = min(tiles, resident CTAs)); flagged
-// tiles go to the EXACT instance of sweep.cuh as before.
+// tiles go to the EXACT instance of sweep.cuh as before.  Each CTA starts
+// on tile blockIdx.x; the elected thread claims the next tile (a global
+// counter, so tiles with a moving edge — dearer — balance across CTAs)
+// when the current one starts and prefetches its fields.
 template <int AXIS, int NP, int TL>
-__global__ void __launch_bounds__(NP * TL, 3)
+__global__ void __launch_bounds__(NP * TL, PPMLR_SWEEP_V2_MINB)
     sweep_kernel_v2(const SweepArgs A, const __grid_constant__ SweepMaps M) {
   extern __shared__ __align__(128) double smem[];
   __shared__ unsigned long long s_err;
   __shared__ __align__(8) unsigned long long s_mbar[2];
+  __shared__ int s_tile[2];
   constexpr int T = slot_stride(NP * TL);
   const int ntiles = A.nseg * A.ngroups * A.no;
-  int t = blockIdx.x;
   if (threadIdx.x == 0) {
     s_err = kNoError;
+    s_tile[0] = blockIdx.x;
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&s_mbar[0])) : "memory");
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&s_mbar[1])) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    if (t < ntiles)
-      tma_load_fields<AXIS, NP, TL>(A, M, tile_of_v2(t, A.nseg, A.ngroups), smem, &s_mbar[0]);
+    if ((int)blockIdx.x < ntiles)
+      tma_load_fields<AXIS, NP, TL>(A, M, tile_of_v2(blockIdx.x, A.nseg, A.ngroups), smem,
+                                    &s_mbar[0]);
   }
   __syncthreads();
 #pragma unroll 1
-  for (int i = 0; t < ntiles; ++i, t += gridDim.x) {
+  for (int i = 0;; ++i) {
     const int buf = i & 1;
+    const int t = s_tile[buf];
+    if (t >= ntiles) break;
     double* FLD = smem + buf * 8 * T;
     const TileId id = tile_of_v2(t, A.nseg, A.ngroups);
     if (threadIdx.x == 0) {
-      const int tn = t + gridDim.x;
+      const int tn = PPMLR_SWEEP_V2_DYN ? (int)gridDim.x + (int)atomicAdd(A.tile_ctr, 1u)
+                                        : t + (int)gridDim.x;
+      s_tile[buf ^ 1] = tn;
       if (tn < ntiles) {
         // the other buffer held the previous tile's result box: its TMA
         // store must have read it before the next tile's fields land there
@@ -396,7 +412,8 @@ __global__ void __launch_bounds__(NP * TL, 3)
     }
     mbar_wait(&s_mbar[buf], (unsigned)(i >> 1) & 1u);
     bool stored = false;
-    const bool bad = sweep_tile_v2<AXIS, NP, TL, MainOps>(A, M, id, smem, FLD, &s_err, stored);
+    const bool bad =
+        sweep_tile_v2<AXIS, NP, TL, MainOps>(A, M, id, smem, FLD, &s_err, stored);
     const bool any_bad = __syncthreads_or(bad);
     if (threadIdx.x == 0) {
       if (stored) {
