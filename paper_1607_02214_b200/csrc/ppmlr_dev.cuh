@@ -15,6 +15,17 @@
 #define PPMLR_KNS strict
 #endif
 
+// Fast-build algebra switches (tuning; each measured on the B200)
+#ifndef PPMLR_FAST_TRACED
+#define PPMLR_FAST_TRACED 0     // fused limiter + parabola means (traced_lr)
+#endif
+#ifndef PPMLR_FAST_SLOPE_SIGN
+#define PPMLR_FAST_SLOPE_SIGN 1 // limited_slope's product test on the sign bits
+#endif
+#ifndef PPMLR_FAST_RCP_SHARE
+#define PPMLR_FAST_RCP_SHARE 1  // one 1/rho per signal speed, rsqrt for 1/sqrt(mu0 rho)
+#endif
+
 namespace ppmlr_b200 {
 
 namespace PPMLR_KNS {
@@ -44,16 +55,28 @@ __device__ __forceinline__ double sclamp(double v, double lo, double hi) {
 }
 
 // physics.cpp:63-72 fast_speed: total field b = B' + bd, |b|^2 in xyz order.
-template <int DIR, class Ops>
+// BD = false: no dipole (the total field is B' itself; no `+ 0.0`).
+template <int DIR, class Ops, bool BD = true>
 __device__ __forceinline__ double fast_speed3(const double* s, double bdx, double bdy,
                                               double bdz, const KC& k, Ops& o) {
-  const double b0 = s[4] + bdx, b1 = s[5] + bdy, b2 = s[6] + bdz;
+  const double b0 = BD ? s[4] + bdx : s[4], b1 = BD ? s[5] + bdy : s[5],
+               b2 = BD ? s[6] + bdz : s[6];
   const double bdir = DIR == 0 ? b0 : (DIR == 1 ? b1 : b2);
-  const double mr = k.c.mu0 * s[0];
-  const double r_mr = o.rcp(mr);
-  const double a2 = o.dv(k.c.gamma * s[7], s[0]);
-  const double ca2 = o.div((b0 * b0 + b1 * b1) + b2 * b2, mr, r_mr);
-  const double can2 = o.div(bdir * bdir, mr, r_mr);
+  double a2, ca2, can2;
+  if constexpr (Ops::kFastMath && PPMLR_FAST_RCP_SHARE) {
+    // one reciprocal: 1/(mu0 rho) = (1/mu0)(1/rho)
+    const double r_rho = o.rcp(s[0]);
+    const double r_mr = k.r_mu0 * r_rho;
+    a2 = (k.c.gamma * s[7]) * r_rho;
+    ca2 = ((b0 * b0 + b1 * b1) + b2 * b2) * r_mr;
+    can2 = (bdir * bdir) * r_mr;
+  } else {
+    const double mr = k.c.mu0 * s[0];
+    const double r_mr = o.rcp(mr);
+    a2 = o.dv(k.c.gamma * s[7], s[0]);
+    ca2 = o.div((b0 * b0 + b1 * b1) + b2 * b2, mr, r_mr);
+    can2 = o.div(bdir * bdir, mr, r_mr);
+  }
   const double sum = a2 + ca2;
   const double disc = o.sq(smax(0.0, sum * sum - (4.0 * a2) * can2));
   return o.sq(0.5 * (sum + disc));
@@ -88,11 +111,21 @@ template <class Ops>
 __device__ __forceinline__ double fast_speed_strip(double rho, double p, double btn,
                                                    double btt1, double btt2, const KC& k,
                                                    Ops& o) {
-  const double mr = k.c.mu0 * rho;
-  const double r_mr = o.rcp(mr);
-  const double a2 = o.dv(k.c.gamma * p, rho);
-  const double ca2 = o.div((btn * btn + btt1 * btt1) + btt2 * btt2, mr, r_mr);
-  const double can2 = o.div(btn * btn, mr, r_mr);
+  double a2, ca2, can2;
+  if constexpr (Ops::kFastMath && PPMLR_FAST_RCP_SHARE) {
+    const double r_rho = o.rcp(rho);
+    const double r_mr = k.r_mu0 * r_rho;
+    a2 = (k.c.gamma * p) * r_rho;
+    const double bn2 = btn * btn;
+    ca2 = ((bn2 + btt1 * btt1) + btt2 * btt2) * r_mr;
+    can2 = bn2 * r_mr;
+  } else {
+    const double mr = k.c.mu0 * rho;
+    const double r_mr = o.rcp(mr);
+    a2 = o.dv(k.c.gamma * p, rho);
+    ca2 = o.div((btn * btn + btt1 * btt1) + btt2 * btt2, mr, r_mr);
+    can2 = o.div(btn * btn, mr, r_mr);
+  }
   const double sum = a2 + ca2;
   const double disc = o.sq(smax(0.0, sum * sum - (4.0 * a2) * can2));
   return o.sq(0.5 * (sum + disc));
@@ -158,7 +191,13 @@ __device__ __forceinline__ double limited_slope(double qm, double q0, double qp,
   const double dq = c0 * (A * dqr + B * dql);
   const double lim = 2.0 * smin(fabs(dql), fabs(dqr));
   const double lim_dq = copysign(smin(fabs(dq), lim), dq);
+#if defined(PPMLR_FAST_MATH) && PPMLR_FAST_SLOPE_SIGN
+  // dqr*dql <= 0 without the FP64 product: opposite sign bits, or a zero
+  // difference (then lim = 0 and lim_dq = +-0)
+  return ((__double2hiint(dql) ^ __double2hiint(dqr)) < 0) ? 0.0 : lim_dq;
+#else
   return (dqr * dql <= 0.0) ? 0.0 : lim_dq;
+#endif
 }
 
 // ppm1d.cpp:217-224 CW84 interface value at edge m (i = m-1) with hoisted e0..e4.
@@ -187,6 +226,30 @@ __device__ __forceinline__ void limit_parabola(double& al, double& ar, double av
   six = 6.0 * (av - 0.5 * (al + ar));
 }
 
+// Fast build: limit_parabola + avg_left/avg_right in one, with the limited
+// six and (ar' - al') selected instead of recomputed (algebraically equal:
+// up -> six = ar'-al' = 3(ar-av); down -> six = -(ar'-al') = 3(al-av);
+// else six = 6(av - (al+ar)/2), ar'-al' = ar-al; flat -> 0), and the
+// steepening test t > d^2/6 taken as 2t > d^2/3 on m2 = 2av - (al+ar).
+__device__ __forceinline__ void traced_lr(double al, double ar, double av, double hs, double tw,
+                                          double r3, double& L, double& R) {
+  const double dr = ar - av, dl = av - al;
+  const bool flat = dr * dl <= 0.0;
+  const double d = ar - al;
+  const double m2 = fma(2.0, av, -(al + ar));
+  const double t2 = d * m2;
+  const double x2 = (d * d) * r3;
+  const bool up = t2 > x2;
+  const bool dn = !up && t2 < -x2;
+  const double av3 = 3.0 * av;
+  const double l = flat ? av : (up ? fma(-2.0, ar, av3) : al);
+  const double r = flat ? av : (dn ? fma(-2.0, al, av3) : ar);
+  const double six = flat ? 0.0 : 3.0 * (up ? dr : (dn ? -dl : m2));
+  const double diff = flat ? 0.0 : (up ? six : (dn ? -six : d));
+  L = fma(hs, fma(tw, six, diff), l);
+  R = fma(-hs, fma(-tw, six, diff), r);
+}
+
 // ppm1d.hpp:20-26 parabola means; hs = 0.5*sigma, tw = 1.0 - (2.0*sigma)/3.0 are
 // shared by every variable with the same sigma (common-subexpression, exact).
 __device__ __forceinline__ double avg_left(double l, double r, double six, double hs,
@@ -204,15 +267,19 @@ __device__ __forceinline__ double tw_of(double sigma, const KC& k, Ops& o) {
 
 // ppm1d.cpp:69-109 solve_edge + edge_flux.  ql/qr strip-frame traced states,
 // bl/br total-field offsets (bd components in strip order a, b, d).
-template <class QL, class QR, class Ops>
+template <class QL, class QR, class Ops, bool BD = true>
 __device__ __forceinline__ double solve_edge(const QL& ql, const QR& qr,
                                              const double* bl, const double* br, const KC& k,
                                              double* f, Ops& o) {
   const Consts& c = k.c;
-  const double wl = ql[kRho] * fast_speed_strip(ql[kRho], ql[kPE], ql[kBn] + bl[0],
-                                                ql[kBt1] + bl[1], ql[kBt2] + bl[2], k, o);
-  const double wr = qr[kRho] * fast_speed_strip(qr[kRho], qr[kPE], qr[kBn] + br[0],
-                                                qr[kBt1] + br[1], qr[kBt2] + br[2], k, o);
+  const double wl =
+      ql[kRho] * (BD ? fast_speed_strip(ql[kRho], ql[kPE], ql[kBn] + bl[0], ql[kBt1] + bl[1],
+                                        ql[kBt2] + bl[2], k, o)
+                     : fast_speed_strip(ql[kRho], ql[kPE], ql[kBn], ql[kBt1], ql[kBt2], k, o));
+  const double wr =
+      qr[kRho] * (BD ? fast_speed_strip(qr[kRho], qr[kPE], qr[kBn] + br[0], qr[kBt1] + br[1],
+                                        qr[kBt2] + br[2], k, o)
+                     : fast_speed_strip(qr[kRho], qr[kPE], qr[kBn], qr[kBt1], qr[kBt2], k, o));
   const double pl = ql[kPE] + o.div((ql[kBt1] * ql[kBt1] + ql[kBt2] * ql[kBt2]) -
                                         ql[kBn] * ql[kBn],
                                     c.two_mu0, k.r_two_mu0);
@@ -225,8 +292,14 @@ __device__ __forceinline__ double solve_edge(const QL& ql, const QR& qr,
   const double pstar = o.div((wr * pl + wl * pr) + (wl * wr) * (ql[kUn] - qr[kUn]), wsum, r_ws);
   const double bn = 0.5 * (ql[kBn] + qr[kBn]);
   const double s = bn < 0.0 ? -1.0 : 1.0;
-  const double al = o.dv(1.0, o.sq(c.mu0 * ql[kRho]));
-  const double ar = o.dv(1.0, o.sq(c.mu0 * qr[kRho]));
+  double al, ar;
+  if constexpr (Ops::kFastMath && PPMLR_FAST_RCP_SHARE) {
+    al = o.rsq(c.mu0 * ql[kRho]);
+    ar = o.rsq(c.mu0 * qr[kRho]);
+  } else {
+    al = o.dv(1.0, o.sq(c.mu0 * ql[kRho]));
+    ar = o.dv(1.0, o.sq(c.mu0 * qr[kRho]));
+  }
   const double asum = al + ar;
   const double r_as = o.rcp(asum);
   const double bt1 = o.div((s * (qr[kUt1] - ql[kUt1]) + ar * qr[kBt1]) + al * ql[kBt1], asum, r_as);

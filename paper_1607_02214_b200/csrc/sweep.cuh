@@ -206,6 +206,24 @@ __device__ __forceinline__ void zone_parabola_dm(const W& q, const D& dm, const 
   limit_parabola(al, ar, q(0), six, k, o);
 }
 
+// The two traced edge states of a zone (P3) from its 3-point window and the
+// stored slopes: the fast build takes the fused limiter (traced_lr).
+template <class W, class D, class Ops>
+__device__ __forceinline__ void zone_traced_dm(const W& q, const D& dm, const double* e0,
+                                               const double* e1, const KC& k, Ops& o,
+                                               double hs, double tw, double& l, double& r) {
+#if defined(PPMLR_FAST_MATH) && PPMLR_FAST_TRACED
+  const double al = interface_value(q(-1), q(0), dm(-1), dm(0), e0);
+  const double ar = interface_value(q(0), q(1), dm(0), dm(1), e1);
+  traced_lr(al, ar, q(0), hs, tw, k.r3, l, r);
+#else
+  double al, ar, six;
+  zone_parabola_dm(q, dm, e0, e1, k, o, al, ar, six);
+  l = avg_left(al, ar, six, hs, tw);
+  r = avg_right(al, ar, six, hs, tw);
+#endif
+}
+
 // Shared slots start on 128-byte boundaries (the TMA destination rule).
 __host__ __device__ constexpr int slot_stride(int cells) { return (cells + 15) & ~15; }
 
@@ -505,15 +523,15 @@ __device__ __forceinline__ bool sweep_tile(const SweepArgs& A, const int seg, co
   auto trace = [&](auto F, const int v, double& l, double& r) {
     const double* pv = NP0 ? SA + fof[v] * T + ci : PRIM + v * T + ci;
     const double av = pv[0];
-    double al = av, ar = av, six = 0.0;
     if (!decltype(F)::value && (kUnswitch || !flat)) {
       const double* dv = SLP + v * T + ci;
       auto win = [&](int j) { return pv[j * SS]; };
       auto dwin = [&](int j) { return dv[j * SS]; };
-      zone_parabola_dm(win, dwin, e0, e1, k, o3, al, ar, six);
+      zone_traced_dm(win, dwin, e0, e1, k, o3, hs, tw, l, r);
+    } else {
+      l = avg_left(av, av, 0.0, hs, tw);
+      r = avg_right(av, av, 0.0, hs, tw);
     }
-    l = avg_left(al, ar, six, hs, tw);
-    r = avg_right(al, ar, six, hs, tw);
   };
   {
   if (XS) {

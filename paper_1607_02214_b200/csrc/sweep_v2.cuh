@@ -82,7 +82,7 @@ __device__ __forceinline__ bool sweep_tile_v2(const SweepArgs& A, const SweepMap
 #pragma unroll
     for (int f = 0; f < 8; ++f) qv[f] = FLD[f * T + ci];
     Ops o;
-    CF[ci] = fast_speed3<AXIS>(qv, 0.0, 0.0, 0.0, k, o);
+    CF[ci] = fast_speed3<AXIS, Ops, false>(qv, 0.0, 0.0, 0.0, k, o);
     tbad |= o.bad;
     if (s >= 1 && s <= TLv - 2) {
       const double* gc = A.slope + 3 * q;
@@ -114,16 +114,15 @@ __device__ __forceinline__ bool sweep_tile_v2(const SweepArgs& A, const SweepMap
     const double tw = tw_of(sigma, k, o);
     auto trace = [&](auto F, const int v, double& l, double& r) {
       const double* pv = FLD + fof[v] * T + ci;
-      const double av = pv[0];
-      double al = av, ar = av, six = 0.0;
       if (!decltype(F)::value) {
         const double* dv = TR + v * T + ci;
         auto win = [&](int j) { return pv[j * SS]; };
         auto dwin = [&](int j) { return dv[j * SS]; };
-        zone_parabola_dm(win, dwin, e0, e1, k, o, al, ar, six);
+        zone_traced_dm(win, dwin, e0, e1, k, o, hs, tw, l, r);
+      } else {  // flat strip-end zone
+        l = pv[0];
+        r = pv[0];
       }
-      l = avg_left(al, ar, six, hs, tw);
-      r = avg_right(al, ar, six, hs, tw);
     };
     auto all8 = [&](auto F) {
       double Lr, Lp;
@@ -161,7 +160,7 @@ __device__ __forceinline__ bool sweep_tile_v2(const SweepArgs& A, const SweepMap
     const double bz[3] = {0.0, 0.0, 0.0};
     const SmemVec qr{LFT + ci + SS, T};
     Ops o;
-    const double us = solve_edge(R, qr, bz, bz, k, f, o);
+    const double us = solve_edge<double[8], SmemVec, Ops, false>(R, qr, bz, bz, k, f, o);
     tbad |= o.bad;
     CF[ci + SS] = us;
     mv = s + 1 >= 4 && s + 1 <= TLv - 4 && us * dt != 0.0;
