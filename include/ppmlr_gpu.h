@@ -252,6 +252,16 @@ struct ppmlr_gpu_options {
 
 int ppmlr_gpu_harness_create(const ppmlr_axis_spec specs[3], int px, int py, int pz,
                              const ppmlr_gpu_options* opts, ppmlr_gpu_harness** out);
+/* The same harness over several GPUs of one process: block r lives on
+ * devices[r % ndevices] (peer access is enabled between them; creation fails
+ * with PPMLR_RUNTIME when a pair has none).  Each block issues on its own
+ * stream; halo copies pull the neighbours' faces over NVLink after their
+ * state events and the global dt is a min over the blocks' device slots, so
+ * a step has no host synchronisation (harness.hpp:79 / harness.cpp:18-28:
+ * the reference keeps every rank in one process too). */
+int ppmlr_gpu_harness_create_on(const ppmlr_axis_spec specs[3], int px, int py, int pz,
+                                const ppmlr_gpu_options* opts, const int* devices,
+                                int ndevices, ppmlr_gpu_harness** out);
 void ppmlr_gpu_harness_destroy(ppmlr_gpu_harness* h);
 /* init_magnetosphere (harness.cpp:30-33, stepper.cpp:83-112) */
 int ppmlr_gpu_harness_init_magnetosphere(ppmlr_gpu_harness* h, double rho_core,

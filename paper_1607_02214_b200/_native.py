@@ -149,6 +149,8 @@ _sig("ppmlr_gpu_sweep_strips", C.c_int, _dp, _dp, _dp, C.c_int, C.c_int, C.c_int
      C.c_double, C.c_double, C.c_double, C.c_double, C.c_int, C.c_int)
 _sig("ppmlr_gpu_harness_create", C.c_int, C.POINTER(AxisSpecC), C.c_int, C.c_int, C.c_int,
      C.POINTER(OptionsC), C.POINTER(_vp))
+_sig("ppmlr_gpu_harness_create_on", C.c_int, C.POINTER(AxisSpecC), C.c_int, C.c_int, C.c_int,
+     C.POINTER(OptionsC), C.POINTER(C.c_int), C.c_int, C.POINTER(_vp))
 _sig("ppmlr_gpu_harness_destroy", None, _vp)
 _sig("ppmlr_gpu_harness_init_magnetosphere", C.c_int, _vp, C.c_double, C.c_double,
      C.c_double, C.c_double)

@@ -255,16 +255,27 @@ class _CudaArray:
 
 
 class Harness:
-    """harness.hpp:48-87 on the GPU: every block of the layout resident on
-    ``options.device``; a whole-domain (1,1,1) layout steps as one CUDA graph."""
+    """harness.hpp:48-87 on the GPU.  Every block of the layout is resident on
+    ``options.device`` or, with ``devices=[...]``, block r on
+    ``devices[r % len(devices)]`` (one process driving several GPUs, peer
+    access over NVLink).  A whole-domain (1,1,1) layout steps as one CUDA
+    graph; multi-block layouts step on per-block streams ordered by events."""
 
-    def __init__(self, specs, partition=(1, 1, 1), options: HarnessOptions | None = None):
+    def __init__(self, specs, partition=(1, 1, 1), options: HarnessOptions | None = None,
+                 devices=None):
         self.specs = list(specs)
         self.partition = tuple(partition)
         self.options = options or HarnessOptions()
         h = C.c_void_p()
-        check(N.lib.ppmlr_gpu_harness_create(_specs3(self.specs), *self.partition,
-                                             C.byref(self.options.c()), C.byref(h)))
+        if devices is None:
+            check(N.lib.ppmlr_gpu_harness_create(_specs3(self.specs), *self.partition,
+                                                 C.byref(self.options.c()), C.byref(h)))
+        else:
+            devs = (C.c_int * len(devices))(*devices)
+            check(N.lib.ppmlr_gpu_harness_create_on(_specs3(self.specs), *self.partition,
+                                                    C.byref(self.options.c()), devs,
+                                                    len(devices), C.byref(h)))
+        self.devices = list(devices) if devices is not None else [self.options.device]
         self.h = h
         self.layout, self.ionosphere_rank = layout(self.specs, self.partition)
 
@@ -324,7 +335,7 @@ class Harness:
     def block(self, rank=0):
         info = self.layout[rank]
         return Block(N.lib.ppmlr_gpu_harness_block(self.h, rank), owner=self, shape=info.n,
-                     ghost=self.options.ghost, device=self.options.device)
+                     ghost=self.options.ghost, device=self.devices[rank % len(self.devices)])
 
     def gather_interior(self):
         nx, ny, nz = (build_axis(s).n for s in self.specs)

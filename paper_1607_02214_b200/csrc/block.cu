@@ -1106,6 +1106,65 @@ int block_upload_streamed(ppmlr_gpu_block* b, const ChunkFill& fill, bool with_b
 }
 
 // Pre-filled sunward shell, fresh error window and step counter.
+// ---------------------------------------------------------------- multi-block
+// Global dt of an in-process multi-block (multi-device) harness: every
+// block's slot holds cfl * its local CFL min; one thread takes the min over
+// all slots (peer loads when the blocks live on other GPUs) and writes it
+// back to every slot.  min commutes with the monotone cfl * x, so this is
+// compute_global_dt (harness.cpp:45-50) bit for bit.
+__global__ void dt_min_all_kernel(double* const* slots, int n) {
+  double m = *slots[0];
+  for (int r = 1; r < n; ++r) m = fmin(m, *slots[r]);
+  for (int r = 0; r < n; ++r) *slots[r] = m;
+}
+
+int launch_dt_min_all(double* const* d_slots, int n, cudaStream_t st) {
+  dt_min_all_kernel<<<1, 1, 0, st>>>(d_slots, n);
+  CK(cudaGetLastError());
+  return 0;
+}
+
+int block_begin_window(ppmlr_gpu_block* b, long first_step) {
+  CK(cudaSetDevice(b->device));
+  unsigned long long init[2] = {kNoError, 0};
+  CK(cudaMemcpyAsync(b->d_err, init, sizeof init, cudaMemcpyHostToDevice, b->stream));
+  b->step_base = first_step;
+  return 0;
+}
+
+int block_read_error(ppmlr_gpu_block* b, unsigned long long* key, unsigned long long* step) {
+  CK(cudaSetDevice(b->device));
+  CK(cudaMemcpyAsync(b->h_pinned + 4, b->d_err, 16, cudaMemcpyDeviceToHost, b->stream));
+  CK(cudaStreamSynchronize(b->stream));
+  std::memcpy(key, b->h_pinned + 4, 8);
+  std::memcpy(step, b->h_pinned + 5, 8);
+  return 0;
+}
+
+int block_last_dt_time(ppmlr_gpu_block* b, double* dt, double* time) {
+  CK(cudaSetDevice(b->device));
+  CK(cudaMemcpyAsync(b->h_pinned + 2, b->d_dt_prev, 8, cudaMemcpyDeviceToHost, b->stream));
+  CK(cudaMemcpyAsync(b->h_pinned + 3, b->d_time, 8, cudaMemcpyDeviceToHost, b->stream));
+  CK(cudaStreamSynchronize(b->stream));
+  *dt = b->h_pinned[2];
+  *time = b->h_pinned[3];
+  return 0;
+}
+
+int block_reset_error(ppmlr_gpu_block* b) {
+  CK(cudaSetDevice(b->device));
+  const unsigned long long reset = kNoError;
+  CK(cudaMemcpy(b->d_err, &reset, 8, cudaMemcpyHostToDevice));
+  return 0;
+}
+
+int block_raise_error(ppmlr_gpu_block* b, unsigned long long key) {
+  std::string msg;
+  const int rc = decode_error(b, key, msg);
+  set_error(msg);
+  return rc;
+}
+
 // ---------------------------------------------------------------- device setup
 // make_block's default state and dipole (stepper.cpp:63-69) and the built-in
 // init_with ICs (harness.cpp:35-43; kinds 0 uniform, 1 Brio-Wu, 2

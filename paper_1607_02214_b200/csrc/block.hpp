@@ -157,4 +157,12 @@ int block_finish_upload(ppmlr_gpu_block* b);
 // bit-identical to the host path; frozen set untouched.
 bool device_init_supported(int kind);
 int block_init_device(ppmlr_gpu_block* b, int kind, const double* params, bool with_bd);
+// Multi-block harness plumbing (block.cu): the global-dt reduction over the
+// blocks' device slots, and the error window / first-failure key of a block.
+int launch_dt_min_all(double* const* d_slots, int n, cudaStream_t st);
+int block_begin_window(ppmlr_gpu_block* b, long first_step);
+int block_read_error(ppmlr_gpu_block* b, unsigned long long* key, unsigned long long* step);
+int block_reset_error(ppmlr_gpu_block* b);
+int block_last_dt_time(ppmlr_gpu_block* b, double* dt, double* time);  // host sync
+int block_raise_error(ppmlr_gpu_block* b, unsigned long long key);
 }  // namespace ppmlr_b200

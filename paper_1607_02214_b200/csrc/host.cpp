@@ -563,7 +563,13 @@ struct ppmlr_gpu_harness {
   std::vector<std::vector<double>> fst;
   long step = 0;
   double time = 0.0;
-  cudaStream_t stream = nullptr;  // one stream orders every block's work
+  // Multi-block layouts: one stream per block (on the block's device),
+  // ordered with events (no host synchronisation inside a step); the global
+  // dt is reduced on block 0's stream over the blocks' device slots.
+  std::vector<int> devices;             // device of each block
+  std::vector<cudaEvent_t> ev_state;    // block r's current state is complete
+  cudaEvent_t ev_dt = nullptr;          // global dt written to every slot
+  double** d_slots = nullptr;           // (block 0's device) each block's dt slot
   uint64_t ledger_bytes = 0;
   long ledger_messages = 0, ledger_events = 0;
   std::vector<LedgerRow> ledger;
@@ -642,25 +648,179 @@ void record_exchange(ppmlr_gpu_harness* h, long step) {
   h->ledger_events += e.copy_events;
 }
 
-// exchange_and_fill (harness.cpp:52-57): halos from neighbours, then
-// physical-face fills, on every block's current buffer.
-int exchange_and_fill(ppmlr_gpu_harness* h) {
-  for (size_t r = 0; r < h->blocks.size(); ++r)
-    for (int face = 0; face < 6; ++face) {
-      const int nb = h->plan[r].neighbor[face];
-      if (nb < 0) continue;
-      if (int rc = ppmlr_gpu_block_copy_face(h->blocks[r], face, h->blocks[nb], kG)) return rc;
+// ---------------------------------------------------------------- multi-block
+// The reference Harness owns every block in one process (harness.hpp:79,
+// harness.cpp:18-28).  Here each block lives on its own device (or several
+// on one), issues on its own stream, and the blocks are ordered by CUDA
+// events only: a halo copy on block r waits for its neighbour's state event,
+// the global dt is a reduction over the blocks' device slots on block 0's
+// stream.  The host synchronises once per advance()/run() window, to read
+// the dt and the blocks' first-failure keys.
+
+void multi_setup(ppmlr_gpu_harness* h) {
+  const size_t nb = h->blocks.size();
+  // peer access between every pair of devices in use (halo copies and the
+  // dt reduction load and store across NVLink)
+  std::vector<int> devs = h->devices;
+  std::sort(devs.begin(), devs.end());
+  devs.erase(std::unique(devs.begin(), devs.end()), devs.end());
+  for (int a : devs)
+    for (int b : devs) {
+      if (a == b) continue;
+      int can = 0;
+      cudaDeviceCanAccessPeer(&can, a, b);
+      if (!can)
+        throw SpecError(PPMLR_RUNTIME, "no peer access from device " + std::to_string(a) +
+                                           " to device " + std::to_string(b));
+      cudaSetDevice(a);
+      const cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+        throw SpecError(PPMLR_RUNTIME, std::string("cudaDeviceEnablePeerAccess: ") +
+                                           cudaGetErrorString(e));
+      cudaGetLastError();
     }
-  record_exchange(h, h->step);
-  for (auto* b : h->blocks)
-    if (int rc = ppmlr_gpu_block_fill_boundaries(b, 7, kG)) return rc;
-  return 0;
+  h->ev_state.resize(nb);
+  for (size_t r = 0; r < nb; ++r) {
+    cudaSetDevice(h->devices[r]);
+    if (cudaEventCreateWithFlags(&h->ev_state[r], cudaEventDisableTiming) != cudaSuccess)
+      throw SpecError(PPMLR_RUNTIME, "cudaEventCreate failed");
+  }
+  cudaSetDevice(h->devices[0]);
+  if (cudaEventCreateWithFlags(&h->ev_dt, cudaEventDisableTiming) != cudaSuccess ||
+      cudaMalloc(&h->d_slots, sizeof(double*) * nb) != cudaSuccess)
+    throw SpecError(PPMLR_RUNTIME, "multi-block setup: allocation failed");
+  std::vector<double*> slots(nb);
+  for (size_t r = 0; r < nb; ++r) slots[r] = ppmlr_gpu_block_dt_slot(h->blocks[r]);
+  if (cudaMemcpy(h->d_slots, slots.data(), sizeof(double*) * nb, cudaMemcpyHostToDevice) !=
+      cudaSuccess)
+    throw SpecError(PPMLR_RUNTIME, "multi-block setup: slot table upload failed");
 }
 
-int check_in_rank_order(ppmlr_gpu_harness* h) {
-  for (auto* b : h->blocks)
-    if (int rc = ppmlr_gpu_block_check(b)) return rc;
-  return 0;
+cudaStream_t stream_of(ppmlr_gpu_harness* h, size_t r) {
+  return static_cast<cudaStream_t>(ppmlr_gpu_block_stream(h->blocks[r]));
+}
+
+#define MK(x)                                                                   \
+  do {                                                                          \
+    const cudaError_t e_ = (x);                                                 \
+    if (e_ != cudaSuccess) throw SpecError(PPMLR_RUNTIME, cudaGetErrorString(e_)); \
+  } while (0)
+
+void record_states(ppmlr_gpu_harness* h) {
+  for (size_t r = 0; r < h->blocks.size(); ++r) {
+    MK(cudaSetDevice(h->devices[r]));
+    MK(cudaEventRecord(h->ev_state[r], stream_of(h, r)));
+  }
+}
+
+// compute_global_dt (harness.cpp:45-50): every slot holds cfl * local min
+void multi_global_dt(ppmlr_gpu_harness* h) {
+  record_states(h);
+  cudaStream_t s0 = stream_of(h, 0);
+  MK(cudaSetDevice(h->devices[0]));
+  for (size_t r = 1; r < h->blocks.size(); ++r) MK(cudaStreamWaitEvent(s0, h->ev_state[r], 0));
+  if (int e = launch_dt_min_all(h->d_slots, (int)h->blocks.size(), s0))
+    throw SpecError(e, ppmlr_gpu_last_error());
+  MK(cudaEventRecord(h->ev_dt, s0));
+  for (size_t r = 1; r < h->blocks.size(); ++r) {
+    MK(cudaSetDevice(h->devices[r]));
+    MK(cudaStreamWaitEvent(stream_of(h, r), h->ev_dt, 0));
+  }
+}
+
+// exchange_step + apply_boundaries (harness.cpp:52-57): each block pulls
+// `layers` ghost layers of the faces in `axis_mask` from its neighbours'
+// current buffers (after their state events), then fills its physical faces.
+// Only what the next kernel reads is copied; the ledger
+// keeps the reference's full-exchange accounting.
+void multi_exchange(ppmlr_gpu_harness* h, int axis_mask, int layers, long step) {
+  record_states(h);
+  for (size_t r = 0; r < h->blocks.size(); ++r) {
+    MK(cudaSetDevice(h->devices[r]));
+    for (int face = 0; face < 6; ++face) {
+      const int nb = h->plan[r].neighbor[face];
+      if (nb < 0 || !((axis_mask >> (face / 2)) & 1)) continue;
+      MK(cudaStreamWaitEvent(stream_of(h, r), h->ev_state[nb], 0));
+      if (int e = ppmlr_gpu_block_copy_face(h->blocks[r], face, h->blocks[nb], layers))
+        throw SpecError(e, ppmlr_gpu_last_error());
+    }
+    if (int e = ppmlr_gpu_block_fill_boundaries(h->blocks[r], axis_mask, layers))
+      throw SpecError(e, ppmlr_gpu_last_error());
+  }
+  record_exchange(h, step);
+}
+
+// The first failure in the reference's order: earliest (step, phase), then
+// the lowest rank (its loops run rank by rank), then the block's own key.
+// A non-finite CFL candidate of the step after the window is deferred to the
+// next advance, like the single-block path (block.cu check_impl).
+int multi_check(ppmlr_gpu_harness* h) {
+  int best = -1;
+  unsigned long long best_key = kNoError, step = 0;
+  for (size_t r = 0; r < h->blocks.size(); ++r) {
+    unsigned long long key = kNoError;
+    if (int e = block_read_error(h->blocks[r], &key, &step)) return e;
+    if (key == kNoError) continue;
+    if (best < 0 || (key >> kErrAxisShift) < (best_key >> kErrAxisShift)) {
+      best = (int)r;
+      best_key = key;
+    }
+  }
+  if (best < 0) return 0;
+  for (auto* b : h->blocks) {
+    block_reset_error(b);
+    b->dt_valid = false;
+  }
+  if (err_phase(best_key) == kPhaseCfl && err_step(best_key) == (step & kErrStepMask)) return 0;
+  return block_raise_error(h->blocks[best], best_key);
+}
+
+// `steps` Harness::advance steps of a multi-block layout, stream-ordered on
+// every block; the dt of the last step is returned in *dt_last.
+int multi_run(ppmlr_gpu_harness* h, long steps, double* dt_last) {
+  static const int order[2][3] = {{0, 1, 2}, {2, 1, 0}};
+  const double cfl = h->o.cfl;
+  const int with_sources = h->o.with_sources;
+  return guarded([&] {
+    // the blocks' local cfl*min, unless the previous window left it for
+    // this state (every block; any upload or step outside clears it)
+    bool valid = true;
+    for (auto* b : h->blocks) valid = valid && b->dt_valid && b->dt_cfl == cfl;
+    for (auto* b : h->blocks) {
+      if (int e = block_begin_window(b, h->step)) throw SpecError(e, ppmlr_gpu_last_error());
+      if (!valid)
+        if (int e = ppmlr_gpu_block_local_dt_async(b, cfl))
+          throw SpecError(e, ppmlr_gpu_last_error());
+    }
+    for (long s = 0; s < steps; ++s) {
+      const int parity = (h->step + s) % 2 == 0 ? 0 : 1;
+      multi_global_dt(h);
+      for (int k = 0; k < 3; ++k) {
+        const int axis = order[parity][k];
+        multi_exchange(h, 1 << axis, kG, h->step + s);
+        for (size_t r = 0; r < h->blocks.size(); ++r)
+          if (int e = ppmlr_gpu_block_sweep_async(h->blocks[r], axis, k))
+            throw SpecError(e, ppmlr_gpu_last_error());
+      }
+      if (with_sources) multi_exchange(h, 7, 1, h->step + s);
+      for (size_t r = 0; r < h->blocks.size(); ++r)
+        if (int e = ppmlr_gpu_block_end_step(h->blocks[r], cfl, with_sources))
+          throw SpecError(e, ppmlr_gpu_last_error());
+    }
+    // dt of the last step: block 0's d_dt_prev, host sync
+    double dt = 0.0, t = 0.0;
+    if (int e = block_last_dt_time(h->blocks[0], &dt, &t))
+      throw SpecError(e, ppmlr_gpu_last_error());
+    if (int e = multi_check(h)) return e;
+    for (auto* b : h->blocks) {  // the fused CFL left the next local cfl*min
+      b->dt_valid = true;
+      b->dt_cfl = cfl;
+    }
+    h->step += steps;
+    h->time = t;
+    if (dt_last) *dt_last = dt;
+    return 0;
+  });
 }
 
 }  // namespace
@@ -778,9 +938,16 @@ uint64_t ppmlr_exchanged_bytes(const ppmlr_axis_spec specs[3], int px, int py, i
 
 int ppmlr_gpu_harness_create(const ppmlr_axis_spec specs[3], int px, int py, int pz,
                              const ppmlr_gpu_options* opts, ppmlr_gpu_harness** out) {
+  return ppmlr_gpu_harness_create_on(specs, px, py, pz, opts, &opts->device, 1, out);
+}
+
+int ppmlr_gpu_harness_create_on(const ppmlr_axis_spec specs[3], int px, int py, int pz,
+                                const ppmlr_gpu_options* opts, const int* devices,
+                                int ndevices, ppmlr_gpu_harness** out) {
   *out = nullptr;
   auto* h = new ppmlr_gpu_harness();
   const int rc = guarded([&] {
+    if (!devices || ndevices < 1) invalid("create_on: empty device list");
     for (int a = 0; a < 3; ++a) h->ax[a] = make_axis(specs[a]);
     h->cnt[0] = px;
     h->cnt[1] = py;
@@ -823,16 +990,11 @@ int ppmlr_gpu_harness_create(const ppmlr_axis_spec specs[3], int px, int py, int
       }
       d.with_dipole = h->o.with_dipole;
       d.precision = h->o.precision;
-      d.device = h->o.device;
+      d.device = devices[r % ndevices];
       ppmlr_gpu_block* b = nullptr;
       if (int e = ppmlr_gpu_block_create(&d, &b)) throw SpecError(e, ppmlr_gpu_last_error());
       h->blocks.push_back(b);
-      if (nb > 1) {  // halo copies read the neighbour's buffers: share one stream
-        if (!h->stream && cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess)
-          throw SpecError(PPMLR_RUNTIME, "cudaStreamCreate failed");
-        if (int e = ppmlr_gpu_block_set_stream(b, h->stream))
-          throw SpecError(e, ppmlr_gpu_last_error());
-      }
+      h->devices.push_back(d.device);
       // make_block's default state {1, 0, 0, 1} and its dipole
       if (use_device_init(-2)) {
         init_device(h, (int)r, -2, nullptr, true);
@@ -842,6 +1004,7 @@ int ppmlr_gpu_harness_create(const ppmlr_axis_spec specs[3], int px, int py, int
         upload_init(h, (int)r, ci, true);
       }
     }
+    if (nb > 1) multi_setup(h);
     return 0;
   });
   if (rc) {
@@ -855,8 +1018,14 @@ int ppmlr_gpu_harness_create(const ppmlr_axis_spec specs[3], int px, int py, int
 void ppmlr_gpu_harness_destroy(ppmlr_gpu_harness* h) {
   if (!h) return;
   if (h->snap_writer.joinable()) h->snap_writer.join();
+  for (size_t r = 0; r < h->ev_state.size(); ++r) {
+    cudaSetDevice(h->devices[r]);
+    cudaEventDestroy(h->ev_state[r]);
+  }
+  if (!h->devices.empty()) cudaSetDevice(h->devices[0]);
+  if (h->ev_dt) cudaEventDestroy(h->ev_dt);
+  if (h->d_slots) cudaFree(h->d_slots);
   for (auto* b : h->blocks) ppmlr_gpu_block_destroy(b);
-  if (h->stream) cudaStreamDestroy(h->stream);
   delete h;
 }
 
@@ -915,8 +1084,6 @@ int ppmlr_gpu_harness_compute_dt(ppmlr_gpu_harness* h, double* dt_out) {
 }
 
 int ppmlr_gpu_harness_advance(ppmlr_gpu_harness* h, double* dt_out) {
-  const int parity = h->step % 2 == 0 ? 0 : 1;
-  static const int order[2][3] = {{0, 1, 2}, {2, 1, 0}};
   double dt = 0.0;
   if (h->blocks.size() == 1) {
     // whole-domain block: the fused, graph-captured device step
@@ -924,28 +1091,11 @@ int ppmlr_gpu_harness_advance(ppmlr_gpu_harness* h, double* dt_out) {
                                          &dt))
       return rc;
     for (int e = 0; e < 3 + (h->o.with_sources ? 1 : 0); ++e) record_exchange(h, h->step);
+    h->step += 1;
+    h->time += dt;
   } else {
-    if (int rc = ppmlr_gpu_harness_compute_dt(h, &dt)) return rc;
-    for (auto* b : h->blocks)
-      if (int rc = block_set_dt(b, dt)) return rc;
-    for (int s = 0; s < 3; ++s) {
-      if (int rc = exchange_and_fill(h)) return rc;
-      for (auto* b : h->blocks)
-        if (int rc = launch_sweep(b, order[parity][s], kPhaseSweep0 + s)) return rc;
-      if (int rc = check_in_rank_order(h)) return rc;
-    }
-    if (h->o.with_sources) {
-      if (int rc = exchange_and_fill(h)) return rc;
-      for (auto* b : h->blocks)
-        if (int rc = launch_sources(b, 0)) return rc;  // frozen core applied in-kernel
-      if (int rc = check_in_rank_order(h)) return rc;
-    } else {
-      for (auto* b : h->blocks)
-        if (int rc = launch_frozen(b)) return rc;
-    }
+    if (int rc = multi_run(h, 1, &dt)) return rc;
   }
-  h->step += 1;
-  h->time += dt;
   if (dt_out) *dt_out = dt;
   return 0;
 }
@@ -962,8 +1112,11 @@ int ppmlr_gpu_harness_run(ppmlr_gpu_harness* h, long steps) {
     h->step += steps;
     return 0;
   }
-  for (long s = 0; s < steps; ++s)
-    if (int rc = ppmlr_gpu_harness_advance(h, nullptr)) return rc;
+  for (long done = 0; done < steps;) {
+    const long k = std::min(steps - done, kMaxStepsPerCheck);
+    if (int rc = multi_run(h, k, nullptr)) return rc;
+    done += k;
+  }
   return 0;
 }
 

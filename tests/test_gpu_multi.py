@@ -1,0 +1,110 @@
+"""The in-process multi-block / multi-device harness (ppmlr_gpu_harness_
+create_on): every block on its own stream, halo copies pulled from the
+neighbours after their state events, the global dt reduced over the blocks'
+device slots, no host synchronisation inside a step.  On a one-GPU box the
+same code runs with every block mapped to device 0; it must equal the
+reference's partitioned Harness (harness.cpp:18-28, 59-92) bit for bit, and
+report the reference's first failure (rank order within the earliest
+phase)."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import bits_equal
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif("not __import__('pyoracle').have_ref()")]
+
+
+def _blast(n):
+    return [(-0.5, 0.5, -0.5, 0.5, 1.0 / n, n, 1.05)] * 3
+
+
+@pytest.mark.parametrize("part,ndev", [((2, 1, 1), 2), ((4, 1, 1), 4), ((8, 1, 1), 3),
+                                       ((2, 3, 3), 5)])
+def test_multi_device_harness_equals_reference(gpu, oracle, part, ndev):
+    from paper_1607_02214_b200.api import AxisSpec, HarnessOptions
+    specs = _blast(32)
+    ic = (gpu.IC_BLAST, (10.0, 0.1, 0.2))
+    ref = oracle.RefHarness(specs, part)
+    ref.init_ic(*ic)
+    h = gpu.Harness([AxisSpec(*s) for s in specs], part, HarnessOptions(), devices=[0] * ndev)
+    h.init_with(*ic)
+    dts_ref = [ref.advance() for _ in range(3)]
+    dts = [h.advance() for _ in range(3)]
+    assert dts == dts_ref
+    for _ in range(4):
+        ref.advance()
+    h.run(4)
+    assert bits_equal(h.gather_interior(), ref.gather())
+    assert h.time() == ref.time() and h.step_count() == ref.step()
+    assert h.ledger() == ref.ledger()
+    assert h.ledger_csv() == ref.ledger_csv()
+
+
+def test_multi_device_magnetosphere_frozen_core(gpu, oracle):
+    from paper_1607_02214_b200.api import AxisSpec, HarnessOptions
+    specs = [(-48.0, 28.8, -48.0, 28.8, 1.2, 64, 1.05),
+             (-21.6, 21.6, -21.6, 21.6, 1.2, 36, 1.05),
+             (-21.6, 21.6, -21.6, 21.6, 1.2, 36, 1.05)]
+    ref = oracle.RefHarness(specs, (4, 1, 1), boundary=2, with_dipole=True)
+    ref.init_magnetosphere()
+    h = gpu.Harness([AxisSpec(*s) for s in specs], (4, 1, 1),
+                    HarnessOptions(boundary=gpu.MAGNETOSPHERE, with_dipole=True),
+                    devices=[0, 0])
+    h.init_magnetosphere()
+    for _ in range(5):
+        ref.advance()
+    h.run(5)
+    assert bits_equal(h.gather_interior(), ref.gather())
+    assert h.time() == ref.time()
+
+
+@pytest.mark.parametrize("part", [(2, 1, 1), (3, 1, 1)])
+def test_multi_block_first_failure_matches_reference(gpu, oracle, part):
+    """Lagrangian interfaces cross (cfl 2.5): the error type and message are
+    the reference's, for the first failing rank of the earliest phase."""
+    from paper_1607_02214_b200.api import AxisSpec, HarnessOptions
+    specs = _blast(18)
+    ic = (gpu.IC_BLAST, (10.0, 0.1, 0.3))
+    ref = oracle.RefHarness(specs, part, cfl=2.5)
+    ref.init_ic(*ic)
+    h = gpu.Harness([AxisSpec(*s) for s in specs], part, HarnessOptions(cfl=2.5),
+                    devices=[0, 0])
+    h.init_with(*ic)
+    err_r = err_g = None
+    for s in range(20):
+        try:
+            ref.advance()
+        except oracle.OracleError as e:
+            err_r = (s, e.msg)
+            break
+    for s in range(20):
+        try:
+            h.advance()
+        except gpu.Error as e:
+            err_g = (s, str(e))
+            break
+    assert err_r is not None
+    assert err_g == err_r
+
+
+def test_multi_block_run_windows_and_cached_dt(gpu):
+    """run(k) in one window equals k advance() calls; an upload between
+    windows drops the cached next dt (every block)."""
+    from paper_1607_02214_b200.api import AxisSpec, HarnessOptions
+    specs = [AxisSpec(*s) for s in _blast(16)]
+    a = gpu.Harness(specs, (2, 1, 1), HarnessOptions(), devices=[0, 0])
+    b = gpu.Harness(specs, (2, 1, 1), HarnessOptions(), devices=[0, 0])
+    for x in (a, b):
+        x.init_with(gpu.IC_BLAST, (10.0, 0.1, 0.2))
+    a.run(5)
+    for _ in range(5):
+        b.advance()
+    assert bits_equal(a.gather_interior(), b.gather_interior()) and a.time() == b.time()
+    a.init_with(gpu.IC_SMOOTH, ())
+    c = gpu.Harness(specs, (2, 1, 1), HarnessOptions(), devices=[0])
+    c.init_with(gpu.IC_SMOOTH, ())
+    assert [a.advance() for _ in range(2)] == [c.advance() for _ in range(2)]
+    assert bits_equal(a.gather_interior(), c.gather_interior())

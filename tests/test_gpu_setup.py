@@ -83,5 +83,8 @@ def test_device_setup_matches_host_block_state(gpu):
     sl = slice(g - 4, None if g == 4 else -(g - 4))
     want_bd = st["bd"][sl, sl, sl]
     assert bits_equal(bd[:, :, :want_bd.shape[2]], want_bd)
-    assert bits_equal(h.block(0).download(), st["fields"])
+    # the interior (the magnetosphere boundary refills the sunward ghost
+    # shell with the wind on upload, which host_block_state does not)
+    ins = slice(g, -g)
+    assert bits_equal(h.block(0).download()[ins, ins, ins], st["fields"][ins, ins, ins])
     h.close()
