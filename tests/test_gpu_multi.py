@@ -21,11 +21,11 @@ def _blast(n):
     return [(-0.5, 0.5, -0.5, 0.5, 1.0 / n, n, 1.05)] * 3
 
 
-@pytest.mark.parametrize("part,ndev", [((2, 1, 1), 2), ((4, 1, 1), 4), ((8, 1, 1), 3),
-                                       ((2, 3, 3), 5)])
-def test_multi_device_harness_equals_reference(gpu, oracle, part, ndev):
+@pytest.mark.parametrize("part,ndev,n", [((2, 1, 1), 2, 32), ((4, 1, 1), 4, 32),
+                                         ((8, 1, 1), 3, 32), ((2, 3, 3), 5, 36)])
+def test_multi_device_harness_equals_reference(gpu, oracle, part, ndev, n):
     from paper_1607_02214_b200.api import AxisSpec, HarnessOptions
-    specs = _blast(32)
+    specs = _blast(n)
     ic = (gpu.IC_BLAST, (10.0, 0.1, 0.2))
     ref = oracle.RefHarness(specs, part)
     ref.init_ic(*ic)
@@ -103,8 +103,12 @@ def test_multi_block_run_windows_and_cached_dt(gpu):
     for _ in range(5):
         b.advance()
     assert bits_equal(a.gather_interior(), b.gather_interior()) and a.time() == b.time()
-    a.init_with(gpu.IC_SMOOTH, ())
+    # c reaches step 5 from a different state, so a stale cached dt in either
+    # would show; the sweep order depends on the step count, hence step 5
     c = gpu.Harness(specs, (2, 1, 1), HarnessOptions(), devices=[0])
+    c.init_with(gpu.IC_BLAST, (3.0, 0.5, 0.3))
+    c.run(5)
+    a.init_with(gpu.IC_SMOOTH, ())
     c.init_with(gpu.IC_SMOOTH, ())
-    assert [a.advance() for _ in range(2)] == [c.advance() for _ in range(2)]
+    assert [a.advance() for _ in range(3)] == [c.advance() for _ in range(3)]
     assert bits_equal(a.gather_interior(), c.gather_interior())
