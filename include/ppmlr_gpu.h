@@ -183,6 +183,13 @@ int ppmlr_gpu_block_copy_face(ppmlr_gpu_block* dst, int face, ppmlr_gpu_block* s
 int ppmlr_gpu_block_begin(ppmlr_gpu_block* b, double cfl, long first_step);
 int ppmlr_gpu_block_sweep_async(ppmlr_gpu_block* b, int axis, int order_index);
 int ppmlr_gpu_block_end_step(ppmlr_gpu_block* b, double cfl, int with_sources);
+/* Split launches for overlapping a halo exchange with the producing kernel:
+ * part 1 updates only the tiles that hold the 4 x-boundary cells of either
+ * side (what an x neighbour reads), part 2 the rest; issue part 1, pack and
+ * send the faces, then part 2 (which completes the sweep / the step).
+ * part 0 = the whole launch (sweep_async / end_step). */
+int ppmlr_gpu_block_sweep_part(ppmlr_gpu_block* b, int axis, int order_index, int part);
+int ppmlr_gpu_block_end_step_part(ppmlr_gpu_block* b, double cfl, int with_sources, int part);
 /* Simulated time accumulated on the device (host sync). */
 int ppmlr_gpu_block_time(ppmlr_gpu_block* b, double* time_out);
 /* Device scalars for external drivers (e.g. an NCCL min all-reduce of dt):

@@ -136,6 +136,8 @@ _sig("ppmlr_gpu_block_local_dt_async", C.c_int, _BP, C.c_double)
 _sig("ppmlr_gpu_block_begin", C.c_int, _BP, C.c_double, C.c_long)
 _sig("ppmlr_gpu_block_sweep_async", C.c_int, _BP, C.c_int, C.c_int)
 _sig("ppmlr_gpu_block_end_step", C.c_int, _BP, C.c_double, C.c_int)
+_sig("ppmlr_gpu_block_sweep_part", C.c_int, _BP, C.c_int, C.c_int, C.c_int)
+_sig("ppmlr_gpu_block_end_step_part", C.c_int, _BP, C.c_double, C.c_int, C.c_int)
 _sig("ppmlr_gpu_block_time", C.c_int, _BP, _dp)
 _sig("ppmlr_gpu_block_stream", _vp, _BP)
 _sig("ppmlr_gpu_block_set_stream", C.c_int, _BP, _vp)

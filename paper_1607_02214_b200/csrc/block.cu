@@ -482,7 +482,13 @@ void choose_sweep_tiles(ppmlr_gpu_block* b) {
 
 namespace ppmlr_b200 {
 
-int launch_sweep(ppmlr_gpu_block* b, int axis, int phase) {
+// The x-boundary split of a launch over `count` x units of `unit` cells.
+static void split_range(int n0, int unit, int count, int& cl, int& cr) {
+  cl = std::min(count, (kG + unit - 1) / unit);
+  cr = std::max(cl, std::min(count, n0 >= kG ? (n0 - kG) / unit : 0));
+}
+
+int launch_sweep(ppmlr_gpu_block* b, int axis, int phase, int part) {
   SweepArgs A{};
   double* in = b->buf[b->cur];
   double* out = b->buf[b->cur ^ 1];
@@ -520,6 +526,11 @@ int launch_sweep(ppmlr_gpu_block* b, int axis, int phase) {
   A.redo_count = b->d_redo;
   A.redo_list = b->d_redo + 1;
   A.tile_ctr = b->d_redo + b->redo_cap + 1;
+  A.part = part;
+  if (axis == 0)
+    split_range(b->n[0], A.L, A.nseg, A.cl, A.cr);
+  else
+    split_range(b->n[0], kSweepNP, A.ngroups, A.cl, A.cr);
   const int T = slot_stride(kSweepNP * (A.L + 8));
   // shared slots per cell: 25 (+3 dipole), 33 with the extra-slot schedule
   // (sweep.cuh XS; with the dipole only in the strict build)
@@ -537,7 +548,7 @@ int launch_sweep(ppmlr_gpu_block* b, int axis, int phase) {
                                             b->sweep_threads[axis], smem, b->stream);
   if (e != cudaSuccess) return cuda_fail(e, "sweep kernel launch");
   b->kernel_launches += 2;  // fast pass + exact re-run of flagged tiles
-  b->cur ^= 1;
+  if (part != 1) b->cur ^= 1;
   return 0;
 }
 
@@ -576,7 +587,7 @@ int launch_cfl(ppmlr_gpu_block* b, unsigned long long step_add) {
   return 0;
 }
 
-int launch_sources(ppmlr_gpu_block* b, int fuse_cfl) {
+int launch_sources(ppmlr_gpu_block* b, int fuse_cfl, int part) {
   SrcArgs A;
   A.in = planes(b->buf[b->cur], b->ncell);
   A.out = planes(b->buf[b->cur ^ 1], b->ncell);
@@ -614,6 +625,9 @@ int launch_sources(ppmlr_gpu_block* b, int fuse_cfl) {
   A.redo_count = b->d_redo;
   A.redo_list = b->d_redo + 1;
   A.redo_cap = b->redo_cap;
+  A.part = part;
+  split_range(b->n[0], PPMLR_KNS::kSrcTX, (b->n[0] + PPMLR_KNS::kSrcTX - 1) / PPMLR_KNS::kSrcTX,
+              A.cl, A.cr);
   CK(cudaMemsetAsync(b->d_redo, 0, sizeof(unsigned), b->stream));
   const cudaError_t e = b->precision == PPMLR_FAST
                             ? launch_sources_fast(A, b->src_maps[b->cur], b->with_dipole,
@@ -622,7 +636,7 @@ int launch_sources(ppmlr_gpu_block* b, int fuse_cfl) {
                                                     b->stream);
   if (e != cudaSuccess) return cuda_fail(e, "sources kernel launch");
   b->kernel_launches += 2;
-  b->cur ^= 1;
+  if (part != 1) b->cur ^= 1;
   return 0;
 }
 
@@ -1540,7 +1554,7 @@ int ppmlr_gpu_block_restore_frozen(ppmlr_gpu_block* b) {
 // One full step of a whole-domain block, stream-ordered, dt already in d_dt.
 // A sweep launch bracketed by CUDA events when timing is on (the dominant
 // kernel's in-run duration for bench.py's roofline).
-static int timed_sweep(ppmlr_gpu_block* b, int axis, int phase) {
+static int timed_sweep(ppmlr_gpu_block* b, int axis, int phase, int part = 0) {
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (b->timing.enabled) {
     auto& t = b->timing;
@@ -1554,7 +1568,7 @@ static int timed_sweep(ppmlr_gpu_block* b, int axis, int phase) {
     t.used += 2;
     CK(cudaEventRecord(e0, b->stream));
   }
-  if (int rc = launch_sweep(b, axis, phase)) return rc;
+  if (int rc = launch_sweep(b, axis, phase, part)) return rc;
   if (e1) CK(cudaEventRecord(e1, b->stream));
   return 0;
 }
@@ -1717,21 +1731,35 @@ int ppmlr_gpu_block_begin(ppmlr_gpu_block* b, double cfl, long first_step) {
 }
 
 int ppmlr_gpu_block_sweep_async(ppmlr_gpu_block* b, int axis, int order_index) {
+  return ppmlr_gpu_block_sweep_part(b, axis, order_index, 0);
+}
+
+int ppmlr_gpu_block_sweep_part(ppmlr_gpu_block* b, int axis, int order_index, int part) {
   b->dt_valid = false;  // state or dt slot changes
   CK(cudaSetDevice(b->device));
-  if (axis < 0 || axis > 2 || order_index < 0 || order_index > 2) {
-    set_error("sweep_async: bad axis/order");
+  if (axis < 0 || axis > 2 || order_index < 0 || order_index > 2 || part < 0 || part > 2) {
+    set_error("sweep_async: bad axis/order/part");
     return PPMLR_INVALID_SPEC;
   }
-  return timed_sweep(b, axis, kPhaseSweep0 + order_index);
+  return timed_sweep(b, axis, kPhaseSweep0 + order_index, part);
 }
 
 int ppmlr_gpu_block_end_step(ppmlr_gpu_block* b, double cfl, int with_sources) {
+  return ppmlr_gpu_block_end_step_part(b, cfl, with_sources, 0);
+}
+
+int ppmlr_gpu_block_end_step_part(ppmlr_gpu_block* b, double cfl, int with_sources, int part) {
   b->dt_valid = false;  // state or dt slot changes
   CK(cudaSetDevice(b->device));
+  if (part < 0 || part > 2) {
+    set_error("end_step: bad part");
+    return PPMLR_INVALID_SPEC;
+  }
   if (with_sources) {
-    if (int rc = launch_sources(b, 1)) return rc;
+    if (int rc = launch_sources(b, 1, part)) return rc;
+    if (part == 1) return 0;  // the interior part closes the step
   } else {
+    if (part == 1) return 0;
     if (int rc = launch_frozen(b)) return rc;
     if (int rc = launch_cfl(b, 1)) return rc;
   }

@@ -134,9 +134,11 @@ cudaError_t launch_sweep_fast(int axis, bool dipole, const SweepArgs& a, const S
 
 namespace ppmlr_b200 {
 // Stream-ordered building blocks of a step (block.cu); used by the harness.
-int launch_sweep(ppmlr_gpu_block* b, int axis, int phase);  // flips b->cur
+// part: 0 every tile, 1 the tiles holding the 4 x-boundary cells of either
+// side, 2 the other tiles (sweep.cuh split_*); parts 0 and 2 flip b->cur.
+int launch_sweep(ppmlr_gpu_block* b, int axis, int phase, int part = 0);
 int launch_bc(ppmlr_gpu_block* b, int axis_mask, int layers);
-int launch_sources(ppmlr_gpu_block* b, int fuse_cfl);      // flips b->cur
+int launch_sources(ppmlr_gpu_block* b, int fuse_cfl, int part = 0);  // same parts
 int launch_frozen(ppmlr_gpu_block* b);
 int launch_cfl(ppmlr_gpu_block* b, unsigned long long step_add);
 int launch_step_end(ppmlr_gpu_block* b, double cfl, int close_step, int have_min);

@@ -60,4 +60,14 @@ __device__ __forceinline__ void block_min_commit(double mn, unsigned long long* 
   }
 }
 
+// Split launches for the halo overlap: a launch over `count` x units (sweep
+// segments / pencil groups / source x tiles) of part 1 covers the boundary
+// units [0, cl) and [cr, count), part 2 the interior [cl, cr), part 0 all.
+__host__ __device__ __forceinline__ int split_count(int part, int cl, int cr, int count) {
+  return part == 1 ? cl + (count - cr) : (part == 2 ? cr - cl : count);
+}
+__host__ __device__ __forceinline__ int split_unit(int part, int cl, int cr, int u) {
+  return part == 1 ? (u < cl ? u : cr + (u - cl)) : (part == 2 ? cl + u : u);
+}
+
 }  // namespace ppmlr_b200

@@ -34,9 +34,13 @@ struct SrcArgs {
   unsigned* redo_count;
   unsigned* redo_list;
   unsigned redo_cap;
+  int part, cl, cr;  // x-tile split of a part launch (sweep.cuh split_*)
 };
 
 namespace PPMLR_KNS {
+
+// the (x, y) tile of sources_tiled_kernel and its halo box (see below)
+constexpr int kSrcTX = 32, kSrcTY = 8, kSrcHX = kSrcTX + 4, kSrcHY = kSrcTY + 2;
 
 #ifdef PPMLR_FAST_MATH
 using SrcOps = FastMathOps;
@@ -224,6 +228,10 @@ __global__ void __launch_bounds__(256, 2) sources_exact_kernel(const SrcArgs A) 
     const int i = (int)(t % L.n0);
     const int j = (int)((t / L.n0) % L.n1);
     const int k = (int)(t / ((long long)L.n0 * L.n1));
+    if (all && A.part) {  // overflow: every cell of this part's x tiles
+      const int xt = i / kSrcTX;
+      if ((A.part == 1) != (xt < A.cl || xt >= A.cr)) continue;
+    }
     double s[8], bo[3], nv[3][2][6], nbd[3][2][3], hm[3], hp[3], den[3], rden[3], q[8];
     gather_stencil<DIPOLE>(A, i, j, k, s, bo, nv, nbd, hm, hp, den, rden);
     ExactOps eo;
@@ -245,7 +253,6 @@ __global__ void __launch_bounds__(256, 2) sources_exact_kernel(const SrcArgs A) 
 // The plane box spans x0-2 .. x0+33: a TMA box must start on a 16-byte
 // boundary in x (an even FP64 coordinate), so the x halo is 2 cells wide on
 // the left (only x0-1 is read) and 2 on the right.
-constexpr int kSrcTX = 32, kSrcTY = 8, kSrcHX = kSrcTX + 4, kSrcHY = kSrcTY + 2;
 constexpr int kSrcSlots = 4;
 // plane-field stride in the ring, padded to 128 B (the TMA destination rule)
 constexpr int kSrcPL = ((kSrcHX * kSrcHY + 15) / 16) * 16;
@@ -270,7 +277,7 @@ __global__ void __launch_bounds__(kSrcTX * kSrcTY, 3)
   const Lay& L = A.L;
   const KC c = make_kc(A.c);
   const int tx = threadIdx.x % kSrcTX, ty = threadIdx.x / kSrcTX;
-  const int x0 = blockIdx.x * kSrcTX, y0 = blockIdx.y * kSrcTY;
+  const int x0 = split_unit(A.part, A.cl, A.cr, blockIdx.x) * kSrcTX, y0 = blockIdx.y * kSrcTY;
   const int z0 = blockIdx.z * zchunk, z1 = min(L.n2, z0 + zchunk);
   const int i = x0 + tx, j = y0 + ty;
   const bool in_xy = i < L.n0 && j < L.n1;

@@ -42,6 +42,7 @@
 #pragma once
 #include <cuda.h>  // CUtensorMap (the maps are encoded on the host, block.cu)
 
+#include "grid_types.cuh"
 #include "ppmlr_dev.cuh"
 
 namespace ppmlr_b200 {
@@ -147,7 +148,14 @@ struct SweepArgs {
   unsigned* redo_count;  // tiles whose fast-path guards failed ...
   unsigned* redo_list;   // ... are re-run exactly by the EXACT instance
   unsigned* tile_ctr;    // persistent schedule (sweep_v2.cuh): tiles claimed so far
+  // Split launches for the halo overlap (dist.py): the tiles' x coordinate
+  // unit (the segment of an x sweep, the pencil group of a y/z sweep) is
+  // "boundary" in [0, cl) and [cr, count) -- it holds one of the 4 x cells
+  // a neighbour needs -- and "interior" in [cl, cr).  part 0: every tile,
+  // 1: boundary units only, 2: interior units only.
+  int part, cl, cr;
 };
+
 
 namespace PPMLR_KNS {
 
@@ -902,21 +910,23 @@ __global__ void __launch_bounds__(NP * kSweepTL, PPMLR_SWEEP_MINB)
   // grid = (nseg, ngroups, no): the tile coordinates need no division.
   // The tile's inputs stream in with TMA (boxes sized to the block's tile).
   constexpr bool kTma = PPMLR_SWEEP_TMA;
+  // the split coordinate (segment for x, pencil group for y/z) of a part launch
+  const int seg = AXIS == 0 ? split_unit(A.part, A.cl, A.cr, blockIdx.x) : (int)blockIdx.x;
+  const int grp = AXIS == 0 ? (int)blockIdx.y : split_unit(A.part, A.cl, A.cr, blockIdx.y);
   if (threadIdx.x == 0) {
     s_err = kNoError;
     if (kTma) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&s_mbar)) : "memory");
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      tma_load_tile<AXIS, DIPOLE, NP, TLC>(A, M, blockIdx.x, blockIdx.y, blockIdx.z, smem,
-                                           &s_mbar);
+      tma_load_tile<AXIS, DIPOLE, NP, TLC>(A, M, seg, grp, blockIdx.z, smem, &s_mbar);
     }
   }
   __syncthreads();
   // store[0]: first smem slot of the staged result box, -1 = no TMA store
   int store[4] = {-1, 0, 0, 0};
   const bool bad = sweep_tile<AXIS, DIPOLE, NP, TLC, MainOps, kTma>(
-      A, blockIdx.x, blockIdx.y, blockIdx.z, smem, &s_err, &s_mbar, store);
+      A, seg, grp, blockIdx.z, smem, &s_err, &s_mbar, store);
   // one closing barrier: the tile's results are in shared memory and its
   // flags are final
   const bool any_bad = __syncthreads_or(bad);
@@ -937,7 +947,7 @@ __global__ void __launch_bounds__(NP * kSweepTL, PPMLR_SWEEP_MINB)
   if (any_bad) {
     if (threadIdx.x == 0)
       A.redo_list[atomicAdd(A.redo_count, 1u)] =
-          blockIdx.x + A.nseg * (blockIdx.y + A.ngroups * blockIdx.z);
+          seg + A.nseg * (grp + A.ngroups * blockIdx.z);
   } else if (threadIdx.x == 0 && s_err != kNoError) {
     atomicMin(A.err, s_err);
   }

@@ -351,9 +351,15 @@ __device__ __forceinline__ void tma_load_fields(const SweepArgs& A, const SweepM
         : "memory");
 }
 
-__device__ __forceinline__ TileId tile_of_v2(int t, int nseg, int ngroups) {
-  const int rest = t / nseg;
-  return {t - rest * nseg, rest % ngroups, rest / ngroups};
+// Tile t of a (part) launch: the split coordinate runs over its part only.
+template <int AXIS>
+__device__ __forceinline__ TileId tile_of_v2(const SweepArgs& A, int t) {
+  const int ns = AXIS == 0 ? split_count(A.part, A.cl, A.cr, A.nseg) : A.nseg;
+  const int ng = AXIS == 0 ? A.ngroups : split_count(A.part, A.cl, A.cr, A.ngroups);
+  const int rest = t / ns;
+  const int u = t - rest * ns, v = rest % ng;
+  return {AXIS == 0 ? split_unit(A.part, A.cl, A.cr, u) : u,
+          AXIS == 0 ? v : split_unit(A.part, A.cl, A.cr, v), rest / ng};
 }
 
 #ifndef PPMLR_SWEEP_V2_MINB
@@ -376,7 +382,8 @@ __global__ void __launch_bounds__(NP * TL, PPMLR_SWEEP_V2_MINB)
   __shared__ __align__(8) unsigned long long s_mbar[2];
   __shared__ int s_tile[2];
   constexpr int T = slot_stride(NP * TL);
-  const int ntiles = A.nseg * A.ngroups * A.no;
+  const int ntiles = (AXIS == 0 ? split_count(A.part, A.cl, A.cr, A.nseg) : A.nseg) *
+                     (AXIS == 0 ? A.ngroups : split_count(A.part, A.cl, A.cr, A.ngroups)) * A.no;
   if (threadIdx.x == 0) {
     s_err = kNoError;
     s_tile[0] = blockIdx.x;
@@ -385,7 +392,7 @@ __global__ void __launch_bounds__(NP * TL, PPMLR_SWEEP_V2_MINB)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     if ((int)blockIdx.x < ntiles)
-      tma_load_fields<AXIS, NP, TL>(A, M, tile_of_v2(blockIdx.x, A.nseg, A.ngroups), smem,
+      tma_load_fields<AXIS, NP, TL>(A, M, tile_of_v2<AXIS>(A, blockIdx.x), smem,
                                     &s_mbar[0]);
   }
   __syncthreads();
@@ -395,7 +402,7 @@ __global__ void __launch_bounds__(NP * TL, PPMLR_SWEEP_V2_MINB)
     const int t = s_tile[buf];
     if (t >= ntiles) break;
     double* FLD = smem + buf * 8 * T;
-    const TileId id = tile_of_v2(t, A.nseg, A.ngroups);
+    const TileId id = tile_of_v2<AXIS>(A, t);
     if (threadIdx.x == 0) {
       const int tn = PPMLR_SWEEP_V2_DYN ? (int)gridDim.x + (int)atomicAdd(A.tile_ctr, 1u)
                                         : t + (int)gridDim.x;
@@ -405,7 +412,7 @@ __global__ void __launch_bounds__(NP * TL, PPMLR_SWEEP_V2_MINB)
         // store must have read it before the next tile's fields land there
         asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        tma_load_fields<AXIS, NP, TL>(A, M, tile_of_v2(tn, A.nseg, A.ngroups),
+        tma_load_fields<AXIS, NP, TL>(A, M, tile_of_v2<AXIS>(A, tn),
                                       smem + (buf ^ 1) * 8 * T, &s_mbar[buf ^ 1]);
       }
     }
@@ -429,8 +436,8 @@ __global__ void __launch_bounds__(NP * TL, PPMLR_SWEEP_V2_MINB)
               : "memory");
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       }
-      if (any_bad)
-        A.redo_list[atomicAdd(A.redo_count, 1u)] = t;
+      if (any_bad)  // the tile's full-grid index (sweep.cuh tile_of)
+        A.redo_list[atomicAdd(A.redo_count, 1u)] = id.seg + A.nseg * (id.grp + A.ngroups * id.oc);
       else if (s_err != kNoError)
         atomicMin(A.err, s_err);
       s_err = kNoError;

@@ -2,22 +2,31 @@
 
 The reference's in-process harness (harness.cpp:59-92, exchange.cpp:93-149)
 becomes a distributed step over torch.distributed (NCCL over NVLink on the
-B200 box, gloo for the CPU tests):
+B200 box; gloo through pinned host buffers for the CPU tests and for several
+ranks sharing one GPU):
 
   dt       <- all_reduce(MIN) of every rank's cfl*min   (compute_global_dt)
   for axis in XYZ / ZYX:
-      halo exchange of the `axis` faces, 4 layers        (exchange_step)
+      halo of the `axis` faces, 4 layers                 (exchange_step)
       physical-face fill along `axis`                    (apply_boundaries)
       sweep                                              (sweep_axis)
-  halo exchange of all faces, 1 layer; fill; sources + frozen core; the
-  next local cfl*min fused into the sources epilogue; all_reduce(MIN)
+  halo of all faces, 1 layer; fill; sources + frozen core; the next local
+  cfl*min fused into the sources epilogue; all_reduce(MIN)
 
 Only what the next kernel reads is exchanged (ghosts are
 pure copies, so this is bit-identical to the reference's 4-layer,
 all-face exchanges; the ledger keeps the reference's accounting).  Slabs
-are packed in the reference's HaloSlab order.  The kernel work of a rank is
-issued on torch's current stream, so NCCL and the kernels are stream-ordered
-with no host synchronisation inside a step.
+are packed in the reference's HaloSlab order.
+
+Overlap.  Every exchange is started by the kernel that produces the state it
+carries, split in two launches (block.cu split_*): part 1 updates only the
+tiles holding the 4 boundary x cells of either side, the faces are packed
+and sent (NCCL on a communication stream), and part 2 -- the interior, ~98%
+of the work at 512^3 -- runs on the compute stream while the halo travels.
+The x halo of a ZYX step's x sweep is produced by its y sweep, the one of an
+XYZ step by the previous step's sources; the 1-layer halo of the sources by
+the z sweep (XYZ) or the x sweep (ZYX).  The receiving rank unpacks right
+before the consumer.  No host synchronisation inside a step on NCCL.
 
 The step logic (``advance``) is written against a small block interface so
 the same code runs with the CUDA block (``DeviceRankBlock``) and, in the CPU
@@ -49,12 +58,21 @@ def face_cells(n, face):
 
 
 class Exchanger:
-    """Halo slabs between neighbour ranks with torch.distributed P2P."""
+    """Halo slabs between neighbour ranks with torch.distributed P2P.
 
-    def __init__(self, info, n, make_buffer, group=None):
+    transport "nccl": device buffers; the send/recv run on a communication
+    stream that waits for the pack only, so they overlap the interior work
+    issued after ``start``; ``finish`` makes the compute stream wait and
+    unpacks.  transport "host": host (pinned, when the block is on a GPU)
+    buffers that the pack/unpack kernels write and read directly; ``start``
+    packs, ``finish`` waits for the pack, exchanges over gloo on the host
+    (while the GPU runs the interior) and unpacks."""
+
+    def __init__(self, info, n, make_buffer, group=None, transport="nccl", timing=False):
         self.info = info
         self.n = n
         self.group = group
+        self.transport = transport
         self.send = {}
         self.recv = {}
         for face in range(6):
@@ -64,47 +82,155 @@ class Exchanger:
                 self.recv[face] = make_buffer(cnt)
         self.messages = 0
         self.bytes_moved = 0
+        self.pending = None
+        self.comm = None
+        self.timing = timing
+        self.halo_events = []  # (start, end) CUDA events around the NCCL ops
+        if transport == "nccl":
+            import torch
+            self.comm = torch.cuda.Stream()
 
-    def exchange(self, blk, faces, layers):
+    def faces(self, faces):
+        return tuple(f for f in faces if self.info.neighbor[f] >= 0)
+
+    def _ops(self, faces, layers):
         import torch.distributed as dist
-        faces = [f for f in faces if self.info.neighbor[f] >= 0]
-        if not faces:
-            return
         ops = []
         for f in faces:
             cnt = face_cells(self.n, f) * layers * 8
-            blk.pack_face(f, layers, self.send[f])
             nb = self.info.neighbor[f]
             ops.append(dist.P2POp(dist.isend, self.send[f][:cnt], nb, self.group))
             ops.append(dist.P2POp(dist.irecv, self.recv[f][:cnt], nb, self.group))
             self.messages += 1
             self.bytes_moved += cnt * 8
-        for r in dist.batch_isend_irecv(ops):
-            r.wait()
+        return ops
+
+    def start(self, blk, faces, layers):
+        """Pack `faces` (those with a neighbour) and put them on the wire."""
+        import torch.distributed as dist
+        faces = self.faces(faces)
+        assert self.pending is None, "one halo exchange in flight at a time"
+        if not faces:
+            return
+        for f in faces:
+            blk.pack_face(f, layers, self.send[f])
+        if self.transport == "nccl":
+            import torch
+            ev = torch.cuda.Event()
+            ev.record()
+            self.comm.wait_event(ev)
+            with torch.cuda.stream(self.comm):
+                e0 = e1 = None
+                if self.timing:
+                    e0 = torch.cuda.Event(enable_timing=True)
+                    e0.record()
+                reqs = dist.batch_isend_irecv(self._ops(faces, layers))
+                if self.timing:
+                    e1 = torch.cuda.Event(enable_timing=True)
+                    e1.record()
+                    self.halo_events.append((e0, e1))
+            self.pending = (faces, layers, reqs)
+        else:
+            ev = blk.record_event()
+            self.pending = (faces, layers, ev)
+
+    def finish(self, blk, faces, layers):
+        """Complete the exchange of `faces` (starting it first if nobody
+        did) and unpack into the ghost shells."""
+        import torch.distributed as dist
+        faces = self.faces(faces)
+        if not faces:
+            return
+        if self.pending is None:
+            self.start(blk, faces, layers)
+        got, lay, h = self.pending
+        assert got == faces and lay == layers, (got, faces, lay, layers)
+        self.pending = None
+        if self.transport == "nccl":
+            for r in h:
+                r.wait()  # the compute stream waits for the NCCL work
+        else:
+            if h is not None:
+                h.synchronize()  # the pack kernels have written the host buffers
+            for r in dist.batch_isend_irecv(self._ops(faces, layers)):
+                r.wait()
         for f in faces:
             blk.unpack_face(f, layers, self.recv[f])
 
+    def exchange(self, blk, faces, layers):
+        self.finish(blk, faces, layers)
 
-def begin(blk, cfl, first_step, group=None):
+    def allreduce_min(self, t):
+        import torch
+        import torch.distributed as dist
+        if self.transport == "nccl" or t.device.type == "cpu":
+            dist.all_reduce(t, op=dist.ReduceOp.MIN, group=self.group)
+        else:  # gloo with a device tensor: through the host
+            h = t.cpu()
+            dist.all_reduce(h, op=dist.ReduceOp.MIN, group=self.group)
+            t.copy_(h)
+        del torch
+
+    def halo_ms(self):
+        """Summed NCCL halo time of the timed exchanges (comm stream events)."""
+        tot = 0.0
+        for e0, e1 in self.halo_events:
+            e1.synchronize()
+            tot += e0.elapsed_time(e1)
+        return tot
+
+
+def begin(blk, cfl, first_step, group=None, ex=None):
     import torch.distributed as dist
     blk.begin(cfl, first_step)
-    dist.all_reduce(blk.dt_tensor(), op=dist.ReduceOp.MIN, group=group)
+    if ex is not None:
+        ex.allreduce_min(blk.dt_tensor())
+    else:
+        dist.all_reduce(blk.dt_tensor(), op=dist.ReduceOp.MIN, group=group)
 
 
-def advance(blk, ex, step, cfl, with_sources, group=None):
+def _produce(blk, ex, launch, faces, layers, overlap):
+    """Run a producing kernel; when its output feeds a halo exchange, split
+    it: boundary tiles, start the exchange, interior tiles."""
+    faces = ex.faces(faces) if faces else ()
+    if faces and overlap and getattr(blk, "splits", False):
+        launch(1)
+        ex.start(blk, faces, layers)
+        launch(2)
+    else:
+        launch(0)
+        if faces:
+            ex.start(blk, faces, layers)
+
+
+def advance(blk, ex, step, cfl, with_sources, group=None, overlap=True):
     """One distributed Harness::advance; the dt slot holds the global dt on
-    entry and the next step's global dt on exit."""
-    import torch.distributed as dist
+    entry and the next step's global dt on exit.  A halo exchange the
+    previous step started (the x faces of this step's first sweep) is
+    finished here."""
+    blk.check_stream()
     order = ORDER[0 if step % 2 == 0 else 1]
-    for s, axis in enumerate(order):
-        ex.exchange(blk, (2 * axis, 2 * axis + 1), 4)
+    next_first_x = ORDER[0 if (step + 1) % 2 == 0 else 1][0] == 0
+    for k, axis in enumerate(order):
+        ex.finish(blk, (2 * axis, 2 * axis + 1), 4)
         blk.fill_boundaries(1 << axis, 4)
-        blk.sweep_async(axis, s)
+        if k < 2:
+            nxt = order[k + 1]
+            need = ((2 * nxt, 2 * nxt + 1), 4)
+        elif with_sources:
+            need = (tuple(range(6)), 1)
+        else:
+            need = (((0, 1) if next_first_x else ()), 4)
+        _produce(blk, ex, lambda part, a=axis, s=k: blk.sweep_part(a, s, part), need[0],
+                 need[1], overlap)
     if with_sources:
-        ex.exchange(blk, range(6), 1)
+        ex.finish(blk, range(6), 1)
         blk.fill_boundaries(7, 1)
-    blk.end_step(cfl, with_sources)
-    dist.all_reduce(blk.dt_tensor(), op=dist.ReduceOp.MIN, group=group)
+        _produce(blk, ex, lambda part: blk.end_step_part(cfl, True, part),
+                 (0, 1) if next_first_x else (), 4, overlap)
+    else:
+        blk.end_step(cfl, False)
+    ex.allreduce_min(blk.dt_tensor())
 
 
 class DeviceRankBlock:
@@ -142,8 +268,8 @@ class DeviceRankBlock:
         check(N.lib.ppmlr_gpu_block_create(C.byref(d), C.byref(h)))
         self.h = h
         self.device = device
-        check(N.lib.ppmlr_gpu_block_set_stream(h, C.c_void_p(
-            torch.cuda.current_stream(device).cuda_stream)))
+        self.stream = torch.cuda.current_stream(device)
+        check(N.lib.ppmlr_gpu_block_set_stream(h, C.c_void_p(self.stream.cuda_stream)))
         self.upload(st["fields"], st["bd"], st["frozen_idx"], st["frozen_states"])
         self._dt = torch.as_tensor(_CudaPtr(N.lib.ppmlr_gpu_block_dt_slot(h), 1),
                                    device=f"cuda:{device}")
@@ -181,11 +307,34 @@ class DeviceRankBlock:
     def fill_boundaries(self, mask, layers):
         self.check_rc(self.N.lib.ppmlr_gpu_block_fill_boundaries(self.h, mask, layers))
 
+    splits = True  # sweep_part / end_step_part: boundary-first split launches
+
     def sweep_async(self, axis, s):
         self.check_rc(self.N.lib.ppmlr_gpu_block_sweep_async(self.h, axis, s))
 
+    def sweep_part(self, axis, s, part):
+        self.check_rc(self.N.lib.ppmlr_gpu_block_sweep_part(self.h, axis, s, part))
+
     def end_step(self, cfl, with_sources):
         self.check_rc(self.N.lib.ppmlr_gpu_block_end_step(self.h, cfl, int(with_sources)))
+
+    def end_step_part(self, cfl, with_sources, part):
+        self.check_rc(self.N.lib.ppmlr_gpu_block_end_step_part(self.h, cfl, int(with_sources),
+                                                               part))
+
+    def record_event(self):
+        import torch
+        ev = torch.cuda.Event()
+        ev.record(self.stream)
+        return ev
+
+    def check_stream(self):
+        """Kernels go to the block's stream and torch's NCCL calls order
+        against torch's current stream: they must be the same."""
+        import torch
+        cur = torch.cuda.current_stream(self.device).cuda_stream
+        assert cur == self.stream.cuda_stream, \
+            "dist.advance must run under the stream the block was created on"
 
     def check(self):
         self.check_rc(self.N.lib.ppmlr_gpu_block_check(self.h))
@@ -205,11 +354,17 @@ class DeviceRankBlock:
         return out
 
 
-def run_rank(blk, ex, steps, first_step, cfl, with_sources, group=None, dt_ready=False):
+def run_rank(blk, ex, steps, first_step, cfl, with_sources, group=None, dt_ready=False,
+             overlap=True):
     if not dt_ready:
-        begin(blk, cfl, first_step, group)
+        begin(blk, cfl, first_step, group, ex)
     for s in range(steps):
-        advance(blk, ex, first_step + s, cfl, with_sources, group)
+        advance(blk, ex, first_step + s, cfl, with_sources, group, overlap)
+    # an exchange started for a step that is not run: drop it (its halo is
+    # re-sent by the next window's first consumer)
+    if ex.pending is not None:
+        faces, layers, _ = ex.pending
+        ex.finish(blk, faces, layers)
 
 
 def _traffic(kind, cells):

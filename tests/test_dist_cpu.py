@@ -78,14 +78,30 @@ class OracleRankBlock:
     def fill_boundaries(self, mask, layers):
         self.blk.apply_boundaries(self.o)
 
+    splits = False  # no boundary-first split launches: exchanges start after the kernel
+
     def sweep_async(self, axis, s):
         self.blk.sweep_axis(axis, float(self._dt[0]), self.c)
+
+    def sweep_part(self, axis, s, part):
+        assert part == 0
+        self.sweep_async(axis, s)
 
     def end_step(self, cfl, with_sources):
         if with_sources:
             self.blk.apply_sources(float(self._dt[0]), self.c)
         self.blk.restore_frozen()
         self._local_dt(cfl)
+
+    def end_step_part(self, cfl, with_sources, part):
+        assert part == 0
+        self.end_step(cfl, with_sources)
+
+    def record_event(self):
+        return None
+
+    def check_stream(self):
+        pass
 
     def interior(self):
         return np.ascontiguousarray(self.blk.interior())
@@ -111,10 +127,9 @@ def _worker(rank, world, port, cfg_name, partition, steps, out_dir):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     cfg = _cfg(configs, cfg_name)
     blk = OracleRankBlock(cfg.specs, partition, cfg.options, rank, cfg.ic)
-    ex = pdist.Exchanger(blk.info, blk.n, lambda n: torch.zeros(n, dtype=torch.float64))
-    pdist.begin(blk, cfg.options.cfl, 0)
-    for s in range(steps):
-        pdist.advance(blk, ex, s, cfg.options.cfl, cfg.options.with_sources)
+    ex = pdist.Exchanger(blk.info, blk.n, lambda n: torch.zeros(n, dtype=torch.float64),
+                         transport="host")
+    pdist.run_rank(blk, ex, steps, 0, cfg.options.cfl, cfg.options.with_sources)
     np.save(os.path.join(out_dir, f"rank{rank}.npy"), blk.interior())
     dist.barrier()
     dist.destroy_process_group()
