@@ -490,8 +490,11 @@ static void split_range(int n0, int unit, int count, int& cl, int& cr) {
 
 int launch_sweep(ppmlr_gpu_block* b, int axis, int phase, int part) {
   SweepArgs A{};
-  double* in = b->buf[b->cur];
-  double* out = b->buf[b->cur ^ 1];
+  // part 1 flips b->cur at once (the neighbour faces are packed from the
+  // new state before part 2 runs); part 2 then reads the other buffer
+  const int src = part == 2 ? b->cur ^ 1 : b->cur;
+  double* in = b->buf[src];
+  double* out = b->buf[src ^ 1];
   for (int f = 0; f < 8; ++f) {
     A.src[f] = in + f * b->ncell;
     A.dst[f] = out + f * b->ncell;
@@ -542,13 +545,13 @@ int launch_sweep(ppmlr_gpu_block* b, int axis, int phase, int part) {
   // The sweep writes only the interior of the output buffer; its ghost
   // shells stay stale until the next fill (every reader fills first).
   cudaError_t e = b->precision == PPMLR_FAST
-                      ? launch_sweep_fast(axis, b->with_dipole, A, b->maps[3 * b->cur + axis],
+                      ? launch_sweep_fast(axis, b->with_dipole, A, b->maps[3 * src + axis],
                                           b->sweep_threads[axis], smem, b->stream)
-                      : launch_sweep_strict(axis, b->with_dipole, A, b->maps[3 * b->cur + axis],
+                      : launch_sweep_strict(axis, b->with_dipole, A, b->maps[3 * src + axis],
                                             b->sweep_threads[axis], smem, b->stream);
   if (e != cudaSuccess) return cuda_fail(e, "sweep kernel launch");
   b->kernel_launches += 2;  // fast pass + exact re-run of flagged tiles
-  if (part != 1) b->cur ^= 1;
+  if (part != 2) b->cur ^= 1;
   return 0;
 }
 
@@ -589,8 +592,9 @@ int launch_cfl(ppmlr_gpu_block* b, unsigned long long step_add) {
 
 int launch_sources(ppmlr_gpu_block* b, int fuse_cfl, int part) {
   SrcArgs A;
-  A.in = planes(b->buf[b->cur], b->ncell);
-  A.out = planes(b->buf[b->cur ^ 1], b->ncell);
+  const int src = part == 2 ? b->cur ^ 1 : b->cur;  // as launch_sweep
+  A.in = planes(b->buf[src], b->ncell);
+  A.out = planes(b->buf[src ^ 1], b->ncell);
   A.L = lay_of(b);
   A.bd0 = b->bd ? b->bd : nullptr;
   A.bd1 = b->bd ? b->bd + b->ncell : nullptr;
@@ -630,13 +634,13 @@ int launch_sources(ppmlr_gpu_block* b, int fuse_cfl, int part) {
               A.cl, A.cr);
   CK(cudaMemsetAsync(b->d_redo, 0, sizeof(unsigned), b->stream));
   const cudaError_t e = b->precision == PPMLR_FAST
-                            ? launch_sources_fast(A, b->src_maps[b->cur], b->with_dipole,
+                            ? launch_sources_fast(A, b->src_maps[src], b->with_dipole,
                                                   b->stream)
-                            : launch_sources_strict(A, b->src_maps[b->cur], b->with_dipole,
+                            : launch_sources_strict(A, b->src_maps[src], b->with_dipole,
                                                     b->stream);
   if (e != cudaSuccess) return cuda_fail(e, "sources kernel launch");
   b->kernel_launches += 2;
-  if (part != 1) b->cur ^= 1;
+  if (part != 2) b->cur ^= 1;
   return 0;
 }
 

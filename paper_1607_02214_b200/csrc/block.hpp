@@ -135,7 +135,9 @@ cudaError_t launch_sweep_fast(int axis, bool dipole, const SweepArgs& a, const S
 namespace ppmlr_b200 {
 // Stream-ordered building blocks of a step (block.cu); used by the harness.
 // part: 0 every tile, 1 the tiles holding the 4 x-boundary cells of either
-// side, 2 the other tiles (sweep.cuh split_*); parts 0 and 2 flip b->cur.
+// side, 2 the other tiles (grid_types.cuh split_*).  Parts 0 and 1 flip
+// b->cur (after part 1 the current buffer holds the new boundary cells, so
+// the faces can be packed); part 2 reads the other buffer and completes it.
 int launch_sweep(ppmlr_gpu_block* b, int axis, int phase, int part = 0);
 int launch_bc(ppmlr_gpu_block* b, int axis_mask, int layers);
 int launch_sources(ppmlr_gpu_block* b, int fuse_cfl, int part = 0);  // same parts
