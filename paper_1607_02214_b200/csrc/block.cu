@@ -846,6 +846,22 @@ int ppmlr_gpu_block_create(const ppmlr_gpu_block_desc* d, ppmlr_gpu_block** out)
     b->h_spacings[a].assign(d->spacings[a] + off, d->spacings[a] + off + span);
     std::vector<double> slope, qfc, hm, hp;
     build_axis_tables(b->h_spacings[a], b->h_centers[a], slope, qfc, hm, hp);
+    if (b->precision == PPMLR_FAST) {
+      // fast build: folded factors (ppmlr_dev.cuh kSlopeN / kQfcN)
+      std::vector<double> s2(2 * span), q3(3 * (span + 1));
+      for (int l = 0; l < span; ++l) {
+        s2[2 * l] = slope[3 * l] * slope[3 * l + 1];
+        s2[2 * l + 1] = slope[3 * l] * slope[3 * l + 2];
+      }
+      for (int m = 0; m <= span; ++m) {
+        const double* e = &qfc[5 * m];
+        q3[3 * m] = e[0] + e[1] * e[2];
+        q3[3 * m + 1] = -(e[1] * e[3]);
+        q3[3 * m + 2] = e[1] * e[4];
+      }
+      slope.swap(s2);
+      qfc.swap(q3);
+    }
     b->ax[a].span = span;
     if ((rc = upload_vec(&b->ax[a].dx, b->h_spacings[a]))) return fail(rc);
     if ((rc = upload_vec(&b->ax[a].slope, slope))) return fail(rc);

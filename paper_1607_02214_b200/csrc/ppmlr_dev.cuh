@@ -200,11 +200,60 @@ __device__ __forceinline__ double limited_slope(double qm, double q0, double qp,
 #endif
 }
 
+// Geometry tables per strip position / edge (block.cu build_axis_tables).
+// Strict: the reference's own factors (limited_slope c0, A, B; CW84 e0..e4).
+// Fast: folded into fewer factors -- slopes (c0 A, c0 B), interface values
+// (e0 + e1 e2, -e1 e3, e1 e4) -- fewer FP64 operations and live registers
+// per zone, same values to rounding.
+#ifdef PPMLR_FAST_MATH
+constexpr int kSlopeN = 2, kQfcN = 3;
+#else
+constexpr int kSlopeN = 3, kQfcN = 5;
+#endif
+struct SlopeC {
+  double c[kSlopeN];
+};
+__device__ __forceinline__ SlopeC slope_coef(const double* t, int q) {
+  SlopeC s;
+#pragma unroll
+  for (int j = 0; j < kSlopeN; ++j) s.c[j] = __ldg(t + kSlopeN * q + j);
+  return s;
+}
+
 // ppm1d.cpp:217-224 CW84 interface value at edge m (i = m-1) with hoisted e0..e4.
 __device__ __forceinline__ double interface_value(double qi, double qi1, double dmi,
                                                   double dmi1, const double* e) {
   const double dqr = qi1 - qi;
   return (qi + e[0] * dqr) + e[1] * ((e[2] * dqr - e[3] * dmi1) + e[4] * dmi);
+}
+
+// The interface value from the block's table entry (strict: e0..e4 in the
+// reference's order; fast: the three folded factors).
+__device__ __forceinline__ double iface(double qi, double qi1, double dmi, double dmi1,
+                                        const double* e) {
+#ifdef PPMLR_FAST_MATH
+  return (qi + e[0] * (qi1 - qi)) + (e[1] * dmi1 + e[2] * dmi);
+#else
+  return interface_value(qi, qi1, dmi, dmi1, e);
+#endif
+}
+
+// limited_slope with the block's table entry for the position.
+__device__ __forceinline__ double slope_with(double qm, double q0, double qp, const SlopeC& s) {
+#ifdef PPMLR_FAST_MATH
+  const double dql = q0 - qm;
+  const double dqr = qp - q0;
+  const double dq = s.c[0] * dqr + s.c[1] * dql;
+  const double lim = 2.0 * smin(fabs(dql), fabs(dqr));
+  const double lim_dq = copysign(smin(fabs(dq), lim), dq);
+#if PPMLR_FAST_SLOPE_SIGN
+  return ((__double2hiint(dql) ^ __double2hiint(dqr)) < 0) ? 0.0 : lim_dq;
+#else
+  return (dqr * dql <= 0.0) ? 0.0 : lim_dq;
+#endif
+#else
+  return limited_slope(qm, q0, qp, s.c[0], s.c[1], s.c[2]);
+#endif
 }
 
 // ppm1d.cpp:232-246 monotonicity limiter, branch-free.  ((-d)*d)/6 equals

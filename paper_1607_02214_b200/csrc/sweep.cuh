@@ -191,15 +191,15 @@ __device__ __forceinline__ TileId tile_of(const SweepArgs& A, int t) {
 // The limited parabola of zone (tile row s) from the 5-point window of one
 // variable: reconstruct() (ppm1d.cpp:200-247) restricted to one zone.
 template <class W, class Ops>
-__device__ __forceinline__ void zone_parabola(const W& q, const double* sc, const double* e0,
+__device__ __forceinline__ void zone_parabola(const W& q, const SlopeC* sc, const double* e0,
                                               const double* e1, const KC& k, Ops& o,
                                               double& al, double& ar, double& six) {
   // q(-2..2); sc: slope coefficients at positions q-1, q, q+1 (3 each)
-  const double dmm = limited_slope(q(-2), q(-1), q(0), sc[0], sc[1], sc[2]);
-  const double dm0 = limited_slope(q(-1), q(0), q(1), sc[3], sc[4], sc[5]);
-  const double dmp = limited_slope(q(0), q(1), q(2), sc[6], sc[7], sc[8]);
-  al = interface_value(q(-1), q(0), dmm, dm0, e0);
-  ar = interface_value(q(0), q(1), dm0, dmp, e1);
+  const double dmm = slope_with(q(-2), q(-1), q(0), sc[0]);
+  const double dm0 = slope_with(q(-1), q(0), q(1), sc[1]);
+  const double dmp = slope_with(q(0), q(1), q(2), sc[2]);
+  al = iface(q(-1), q(0), dmm, dm0, e0);
+  ar = iface(q(0), q(1), dm0, dmp, e1);
   limit_parabola(al, ar, q(0), six, k, o);
 }
 
@@ -209,8 +209,8 @@ template <class W, class D, class Ops>
 __device__ __forceinline__ void zone_parabola_dm(const W& q, const D& dm, const double* e0,
                                                  const double* e1, const KC& k, Ops& o,
                                                  double& al, double& ar, double& six) {
-  al = interface_value(q(-1), q(0), dm(-1), dm(0), e0);
-  ar = interface_value(q(0), q(1), dm(0), dm(1), e1);
+  al = iface(q(-1), q(0), dm(-1), dm(0), e0);
+  ar = iface(q(0), q(1), dm(0), dm(1), e1);
   limit_parabola(al, ar, q(0), six, k, o);
 }
 
@@ -221,8 +221,8 @@ __device__ __forceinline__ void zone_traced_dm(const W& q, const D& dm, const do
                                                const double* e1, const KC& k, Ops& o,
                                                double hs, double tw, double& l, double& r) {
 #if defined(PPMLR_FAST_MATH) && PPMLR_FAST_TRACED
-  const double al = interface_value(q(-1), q(0), dm(-1), dm(0), e0);
-  const double ar = interface_value(q(0), q(1), dm(0), dm(1), e1);
+  const double al = iface(q(-1), q(0), dm(-1), dm(0), e0);
+  const double ar = iface(q(0), q(1), dm(0), dm(1), e1);
   traced_lr(al, ar, q(0), hs, tw, k.r3, l, r);
 #else
   double al, ar, six;
@@ -399,12 +399,11 @@ __device__ __forceinline__ bool sweep_tile(const SweepArgs& A, const int seg, co
     if (F01 && s >= 1 && s <= TLv - 2) {
       // P1 fused: the neighbours' strip-frame primitives straight from the
       // TMA'd fields (PRIM is a pure permutation of them) -> TR
-      const double* gc = A.slope + 3 * q;
-      const double c0 = __ldg(gc), cA = __ldg(gc + 1), cB = __ldg(gc + 2);
+      const SlopeC sc = slope_coef(A.slope, q);
 #pragma unroll
       for (int v = 0; v < 8; ++v) {
         const double* pv = SA + fof[v] * T + ci;
-        TR[v * T + ci] = limited_slope(pv[-SS], w[v], pv[SS], c0, cA, cB);
+        TR[v * T + ci] = slope_with(pv[-SS], w[v], pv[SS], sc);
       }
     }
   }
@@ -412,12 +411,11 @@ __device__ __forceinline__ bool sweep_tile(const SweepArgs& A, const int seg, co
 
   // ---- P1: primitive slopes at s in [1, TLv-2] -> SA ---------------------
   if (!F01 && live && s >= 1 && s <= TLv - 2) {
-    const double* gc = A.slope + 3 * q;
-    const double c0 = __ldg(gc), cA = __ldg(gc + 1), cB = __ldg(gc + 2);
+    const SlopeC sc = slope_coef(A.slope, q);
 #pragma unroll
     for (int v = 0; v < 8; ++v) {
       const double* pv = PRIM + v * T + ci;
-      SA[v * T + ci] = limited_slope(pv[-SS], pv[0], pv[SS], c0, cA, cB);
+      SA[v * T + ci] = slope_with(pv[-SS], pv[0], pv[SS], sc);
     }
   }
   if (!F01) __syncthreads();
@@ -430,14 +428,14 @@ __device__ __forceinline__ bool sweep_tile(const SweepArgs& A, const int seg, co
   constexpr bool EO = XS && PPMLR_SWEEP_EDGE_ONCE;
   if (EO) {
     if (live && s >= 1 && s <= zmax && q <= nn - 3) {
-      double e[5];
+      double e[kQfcN];
 #pragma unroll
-      for (int j = 0; j < 5; ++j) e[j] = __ldg(A.qfc + 5 * (q + 1) + j);
+      for (int j = 0; j < kQfcN; ++j) e[j] = __ldg(A.qfc + kQfcN * (q + 1) + j);
 #pragma unroll
       for (int v = 0; v < 8; ++v) {
         const double* pv = PRIM + v * T + ci;
         const double* dv = SA + v * T + ci;
-        TR[v * T + ci] = interface_value(pv[0], pv[SS], dv[0], dv[SS], e);
+        TR[v * T + ci] = iface(pv[0], pv[SS], dv[0], dv[SS], e);
       }
     }
     __syncthreads();
@@ -504,15 +502,15 @@ __device__ __forceinline__ bool sweep_tile(const SweepArgs& A, const int seg, co
   // that only eight traced values are held across a barrier.  The first
   // half holds rho and p, which decide the reference's fallback to the
   // zone's own state for all eight.
-  double e0[5], e1[5], hs = 0.0, tw = 0.0;
+  double e0[kQfcN], e1[kQfcN], hs = 0.0, tw = 0.0;
   bool badL = false, badR = false;
   Ops o3;
   if (z3) {
     if (!flat) {
 #pragma unroll
-      for (int j = 0; j < 5; ++j) {
-        e0[j] = __ldg(A.qfc + 5 * q + j);
-        e1[j] = __ldg(A.qfc + 5 * (q + 1) + j);
+      for (int j = 0; j < kQfcN; ++j) {
+        e0[j] = __ldg(A.qfc + kQfcN * q + j);
+        e1[j] = __ldg(A.qfc + kQfcN * (q + 1) + j);
       }
     }
     const double sigma =
@@ -726,12 +724,11 @@ __device__ __forceinline__ bool sweep_tile(const SweepArgs& A, const int seg, co
     // ---- P7b in P7's phase: conserved slopes -> TR (dead since P3; CONS
     // is untouched by P7), only in tiles with a moving edge
     if (moving && live && s >= 1 && s <= TLv - 2) {
-      const double* gc = A.slope + 3 * q;
-      const double c0 = __ldg(gc), cA = __ldg(gc + 1), cB = __ldg(gc + 2);
+      const SlopeC sc = slope_coef(A.slope, q);
 #pragma unroll
       for (int v = 0; v < 8; ++v) {
         const double* cv = CONS + v * T + ci;
-        TR[v * T + ci] = limited_slope(cv[-SS], cv[0], cv[SS], c0, cA, cB);
+        TR[v * T + ci] = slope_with(cv[-SS], cv[0], cv[SS], sc);
       }
     }
     __syncthreads();
@@ -742,12 +739,11 @@ __device__ __forceinline__ bool sweep_tile(const SweepArgs& A, const int seg, co
   // across the CTA, so the extra barrier is legal.
   if (__syncthreads_or(e8 && CF[ci] * dt != 0.0)) {
     if (live && s >= 1 && s <= TLv - 2) {
-      const double* gc = A.slope + 3 * q;
-      const double c0 = __ldg(gc), cA = __ldg(gc + 1), cB = __ldg(gc + 2);
+      const SlopeC sc = slope_coef(A.slope, q);
 #pragma unroll
       for (int v = 0; v < 8; ++v) {
         const double* cv = CONS + v * T + ci;
-        SA[v * T + ci] = limited_slope(cv[-SS], cv[0], cv[SS], c0, cA, cB);
+        SA[v * T + ci] = slope_with(cv[-SS], cv[0], cv[SS], sc);
       }
     }
     __syncthreads();
@@ -768,16 +764,16 @@ __device__ __forceinline__ bool sweep_tile(const SweepArgs& A, const int seg, co
       const int kc = right ? ci - SS : ci;  // upwind zone
       const int kq = right ? q - 1 : q;
       const double width = __ldg(A.dx + kq) + dt * (CF[kc + SS] - CF[kc]);
-      double e0[5], e1[5];
+      double e0[kQfcN], e1[kQfcN];
 #if !PPMLR_SWEEP_CSLOPE
-      double sc[9];
+      SlopeC sc[3];
 #pragma unroll
-      for (int j = 0; j < 9; ++j) sc[j] = __ldg(A.slope + 3 * (kq - 1) + j);
+      for (int j = 0; j < 3; ++j) sc[j] = slope_coef(A.slope, kq - 1 + j);
 #endif
 #pragma unroll
-      for (int j = 0; j < 5; ++j) {
-        e0[j] = __ldg(A.qfc + 5 * kq + j);
-        e1[j] = __ldg(A.qfc + 5 * (kq + 1) + j);
+      for (int j = 0; j < kQfcN; ++j) {
+        e0[j] = __ldg(A.qfc + kQfcN * kq + j);
+        e1[j] = __ldg(A.qfc + kQfcN * (kq + 1) + j);
       }
       Ops o;
       const double sigma = o.dv(right ? delta : -delta, width);

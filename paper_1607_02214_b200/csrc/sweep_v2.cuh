@@ -85,12 +85,11 @@ __device__ __forceinline__ bool sweep_tile_v2(const SweepArgs& A, const SweepMap
     CF[ci] = fast_speed3<AXIS, Ops, false>(qv, 0.0, 0.0, 0.0, k, o);
     tbad |= o.bad;
     if (s >= 1 && s <= TLv - 2) {
-      const double* gc = A.slope + 3 * q;
-      const double c0 = __ldg(gc), cA = __ldg(gc + 1), cB = __ldg(gc + 2);
+      const SlopeC sc = slope_coef(A.slope, q);
 #pragma unroll
       for (int v = 0; v < 8; ++v) {
         const double* pv = FLD + fof[v] * T + ci;
-        TR[v * T + ci] = limited_slope(pv[-SS], pv[0], pv[SS], c0, cA, cB);
+        TR[v * T + ci] = slope_with(pv[-SS], pv[0], pv[SS], sc);
       }
     }
   }
@@ -101,11 +100,11 @@ __device__ __forceinline__ bool sweep_tile_v2(const SweepArgs& A, const SweepMap
   const bool z3 = live && s >= 2 && s <= zmax;
   if (z3) {
     const bool flat = q >= nn - 2;
-    double e0[5], e1[5];
+    double e0[kQfcN], e1[kQfcN];
 #pragma unroll
-    for (int j = 0; j < 5; ++j) {
-      e0[j] = __ldg(A.qfc + 5 * q + j);
-      e1[j] = __ldg(A.qfc + 5 * (q + 1) + j);
+    for (int j = 0; j < kQfcN; ++j) {
+      e0[j] = __ldg(A.qfc + kQfcN * q + j);
+      e1[j] = __ldg(A.qfc + kQfcN * (q + 1) + j);
     }
     Ops o;
     const double sigma =
@@ -225,12 +224,11 @@ __device__ __forceinline__ bool sweep_tile_v2(const SweepArgs& A, const SweepMap
   if (moving) {
     // ---- P7b: conserved slopes at [1, TLv-2] -> TR (fluxes dead) ----------
     if (live && s >= 1 && s <= TLv - 2) {
-      const double* gc = A.slope + 3 * q;
-      const double c0 = __ldg(gc), cA = __ldg(gc + 1), cB = __ldg(gc + 2);
+      const SlopeC sc = slope_coef(A.slope, q);
 #pragma unroll
       for (int v = 0; v < 8; ++v) {
         const double* cv = FLD + v * T + ci;
-        TR[v * T + ci] = limited_slope(cv[-SS], cv[0], cv[SS], c0, cA, cB);
+        TR[v * T + ci] = slope_with(cv[-SS], cv[0], cv[SS], sc);
       }
     }
     __syncthreads();
@@ -245,11 +243,11 @@ __device__ __forceinline__ bool sweep_tile_v2(const SweepArgs& A, const SweepMap
         const int kc = right ? ci - SS : ci;  // upwind zone
         const int kq = right ? q - 1 : q;
         const double width = __ldg(A.dx + kq) + dt * (CF[kc + SS] - CF[kc]);
-        double e0[5], e1[5];
+        double e0[kQfcN], e1[kQfcN];
 #pragma unroll
-        for (int j = 0; j < 5; ++j) {
-          e0[j] = __ldg(A.qfc + 5 * kq + j);
-          e1[j] = __ldg(A.qfc + 5 * (kq + 1) + j);
+        for (int j = 0; j < kQfcN; ++j) {
+          e0[j] = __ldg(A.qfc + kQfcN * kq + j);
+          e1[j] = __ldg(A.qfc + kQfcN * (kq + 1) + j);
         }
         Ops o;
         const double sigma = o.dv(right ? delta : -delta, width);
