@@ -378,40 +378,47 @@ __global__ void __launch_bounds__(NP * TL, PPMLR_SWEEP_V2_MINB)
   extern __shared__ __align__(128) double smem[];
   __shared__ unsigned long long s_err;
   __shared__ __align__(8) unsigned long long s_mbar[2];
-  __shared__ int s_tile[2];
+  // the claimed tile of each buffer, decoded once by the elected thread:
+  // {t, seg, grp, oc}
+  __shared__ int s_tile[2][4];
   constexpr int T = slot_stride(NP * TL);
   const int ntiles = (AXIS == 0 ? split_count(A.part, A.cl, A.cr, A.nseg) : A.nseg) *
                      (AXIS == 0 ? A.ngroups : split_count(A.part, A.cl, A.cr, A.ngroups)) * A.no;
+  auto claim = [&](int slot, int t) {  // elected thread
+    const TileId id = tile_of_v2<AXIS>(A, t < ntiles ? t : 0);
+    s_tile[slot][0] = t;
+    s_tile[slot][1] = id.seg;
+    s_tile[slot][2] = id.grp;
+    s_tile[slot][3] = id.oc;
+    return id;
+  };
   if (threadIdx.x == 0) {
     s_err = kNoError;
-    s_tile[0] = blockIdx.x;
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&s_mbar[0])) : "memory");
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&s_mbar[1])) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    if ((int)blockIdx.x < ntiles)
-      tma_load_fields<AXIS, NP, TL>(A, M, tile_of_v2<AXIS>(A, blockIdx.x), smem,
-                                    &s_mbar[0]);
+    const TileId id0 = claim(0, blockIdx.x);
+    if ((int)blockIdx.x < ntiles) tma_load_fields<AXIS, NP, TL>(A, M, id0, smem, &s_mbar[0]);
   }
   __syncthreads();
 #pragma unroll 1
   for (int i = 0;; ++i) {
     const int buf = i & 1;
-    const int t = s_tile[buf];
+    const int t = s_tile[buf][0];
     if (t >= ntiles) break;
     double* FLD = smem + buf * 8 * T;
-    const TileId id = tile_of_v2<AXIS>(A, t);
+    const TileId id = {s_tile[buf][1], s_tile[buf][2], s_tile[buf][3]};
     if (threadIdx.x == 0) {
       const int tn = PPMLR_SWEEP_V2_DYN ? (int)gridDim.x + (int)atomicAdd(A.tile_ctr, 1u)
                                         : t + (int)gridDim.x;
-      s_tile[buf ^ 1] = tn;
+      const TileId idn = claim(buf ^ 1, tn);
       if (tn < ntiles) {
         // the other buffer held the previous tile's result box: its TMA
         // store must have read it before the next tile's fields land there
         asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        tma_load_fields<AXIS, NP, TL>(A, M, tile_of_v2<AXIS>(A, tn),
-                                      smem + (buf ^ 1) * 8 * T, &s_mbar[buf ^ 1]);
+        tma_load_fields<AXIS, NP, TL>(A, M, idn, smem + (buf ^ 1) * 8 * T, &s_mbar[buf ^ 1]);
       }
     }
     mbar_wait(&s_mbar[buf], (unsigned)(i >> 1) & 1u);
