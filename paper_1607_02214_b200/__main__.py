@@ -2,6 +2,7 @@
 
     python -m paper_1607_02214_b200 run --config mag160 --steps 20 --cadence 10 --out out/
     python -m paper_1607_02214_b200 verify [all|sod|briowu|convergence|conservation|partition]
+    python -m paper_1607_02214_b200 report [--steps 5] [--transport direct|staged]
 
 Errors print one ``error: ...`` line and exit 1, like the reference CLI
 (ppmlr_main.cpp:185-188).
@@ -41,9 +42,16 @@ def main(argv=None):
     v = sub.add_parser("verify", help="the reference's physics suites on the GPU")
     v.add_argument("suite", nargs="?", default="all")
     v.add_argument("--precision", default="strict", choices=["strict", "fast"])
+    rp = sub.add_parser("report", help="live runs of the reference partition shapes (CSV)")
+    rp.add_argument("--steps", type=int, default=5)
+    rp.add_argument("--transport", default="direct", choices=["direct", "staged"])
     a = ap.parse_args(argv)
     from .api import Error
     try:
+        if a.cmd == "report":
+            from .report import cmd_report
+            cmd_report(a.steps, a.transport)
+            return 0
         if a.cmd == "run":
             from .run import cmd_run
             cmd_run(_config(a.config, a.precision), a.steps, a.cadence, a.out)

@@ -6,7 +6,10 @@
 #endif
 #define PPMLR_KNS fast
 #ifndef PPMLR_SWEEP_V2_ON
-#define PPMLR_SWEEP_V2_ON 1  // sweep_v2.cuh schedule for the no-dipole compile-time tile
+#define PPMLR_SWEEP_V2_ON 1  // sweep_v2.cuh schedule for the compile-time tile
+#endif
+#ifndef PPMLR_SWEEP_V2_DIPOLE
+#define PPMLR_SWEEP_V2_DIPOLE 1  // ... with the dipole too (B_d read from global memory)
 #endif
 #define PPMLR_LAUNCH_NAME launch_sweep_fast
 #include "sweep_launch.inc"

@@ -33,7 +33,7 @@
 namespace ppmlr_b200 {
 namespace PPMLR_KNS {
 
-template <int AXIS, int NP, int TL, class Ops>
+template <int AXIS, bool DIPOLE, int NP, int TL, class Ops>
 __device__ __forceinline__ bool sweep_tile_v2(const SweepArgs& A, const SweepMaps& M,
                                               const TileId id, double* smem, double* FLD,
                                               unsigned long long* s_err, bool& stored) {
@@ -82,7 +82,14 @@ __device__ __forceinline__ bool sweep_tile_v2(const SweepArgs& A, const SweepMap
 #pragma unroll
     for (int f = 0; f < 8; ++f) qv[f] = FLD[f * T + ci];
     Ops o;
-    CF[ci] = fast_speed3<AXIS, Ops, false>(qv, 0.0, 0.0, 0.0, k, o);
+    if (DIPOLE) {  // B_d from global memory (L1/L2: 3 planes, read twice per sweep)
+      const long long off = (long long)(g0 + p + 4) * A.stride_g +
+                            (long long)(oc + 4) * A.stride_o + (long long)q * A.stride_a;
+      CF[ci] = fast_speed3<AXIS, Ops, true>(qv, __ldg(A.bd[0] + off), __ldg(A.bd[1] + off),
+                                            __ldg(A.bd[2] + off), k, o);
+    } else {
+      CF[ci] = fast_speed3<AXIS, Ops, false>(qv, 0.0, 0.0, 0.0, k, o);
+    }
     tbad |= o.bad;
     if (s >= 1 && s <= TLv - 2) {
       const SlopeC sc = slope_coef(A.slope, q);
@@ -156,10 +163,21 @@ __device__ __forceinline__ bool sweep_tile_v2(const SweepArgs& A, const SweepMap
   bool mv = false;
   if (live && s >= 2 && s <= zmax - 1) {
     double f[8];
-    const double bz[3] = {0.0, 0.0, 0.0};
+    double bl[3] = {0.0, 0.0, 0.0}, br[3] = {0.0, 0.0, 0.0};
+    if (DIPOLE) {  // the two zones' B_d in strip order (a, b, d)
+      const long long off = (long long)(g0 + p + 4) * A.stride_g +
+                            (long long)(oc + 4) * A.stride_o + (long long)q * A.stride_a;
+      constexpr int ja = AXIS, jb = (AXIS + 1) % 3, jd = (AXIS + 2) % 3;
+      bl[0] = __ldg(A.bd[ja] + off);
+      bl[1] = __ldg(A.bd[jb] + off);
+      bl[2] = __ldg(A.bd[jd] + off);
+      br[0] = __ldg(A.bd[ja] + off + A.stride_a);
+      br[1] = __ldg(A.bd[jb] + off + A.stride_a);
+      br[2] = __ldg(A.bd[jd] + off + A.stride_a);
+    }
     const SmemVec qr{LFT + ci + SS, T};
     Ops o;
-    const double us = solve_edge<double[8], SmemVec, Ops, false>(R, qr, bz, bz, k, f, o);
+    const double us = solve_edge<double[8], SmemVec, Ops, DIPOLE>(R, qr, bl, br, k, f, o);
     tbad |= o.bad;
     CF[ci + SS] = us;
     mv = s + 1 >= 4 && s + 1 <= TLv - 4 && us * dt != 0.0;
@@ -372,7 +390,7 @@ __device__ __forceinline__ TileId tile_of_v2(const SweepArgs& A, int t) {
 // on tile blockIdx.x; the elected thread claims the next tile (a global
 // counter, so tiles with a moving edge — dearer — balance across CTAs)
 // when the current one starts and prefetches its fields.
-template <int AXIS, int NP, int TL>
+template <int AXIS, bool DIPOLE, int NP, int TL>
 __global__ void __launch_bounds__(NP * TL, PPMLR_SWEEP_V2_MINB)
     sweep_kernel_v2(const SweepArgs A, const __grid_constant__ SweepMaps M) {
   extern __shared__ __align__(128) double smem[];
@@ -424,7 +442,7 @@ __global__ void __launch_bounds__(NP * TL, PPMLR_SWEEP_V2_MINB)
     mbar_wait(&s_mbar[buf], (unsigned)(i >> 1) & 1u);
     bool stored = false;
     const bool bad =
-        sweep_tile_v2<AXIS, NP, TL, MainOps>(A, M, id, smem, FLD, &s_err, stored);
+        sweep_tile_v2<AXIS, DIPOLE, NP, TL, MainOps>(A, M, id, smem, FLD, &s_err, stored);
     const bool any_bad = __syncthreads_or(bad);
     if (threadIdx.x == 0) {
       if (stored) {

@@ -112,3 +112,34 @@ def test_multi_block_run_windows_and_cached_dt(gpu):
     c.init_with(gpu.IC_SMOOTH, ())
     assert [a.advance() for _ in range(3)] == [c.advance() for _ in range(3)]
     assert bits_equal(a.gather_interior(), c.gather_interior())
+
+
+def test_report_rows_match_reference_accounting(gpu, oracle):
+    """`report` (ppmlr_main.cpp:107-139) on the GPU path: every reference
+    partition shape runs live on the multi-block harness; the ledger bytes
+    per step equal the reference Harness's, the state after the steps is
+    bit-identical to the reference's from the same initial arrays, and the
+    modelled speedup is perfmodel.cpp's (mas 4.8828125 x 0.732, capped by the
+    64^3 utilisation floor)."""
+    from paper_1607_02214_b200 import report
+    from paper_1607_02214_b200.api import HarnessOptions
+    rows = report.cmd_report(steps=2, out=lambda line: None)
+    assert [r[:3] for r in rows] == report.REFERENCE_CONFIGS
+    specs = [(-4.8, 4.8, -4.8, 4.8, 0.4, 24, 1.05), (-6.0, 6.0, -6.0, 6.0, 0.4, 30, 1.05),
+             (-6.0, 6.0, -6.0, 6.0, 0.4, 30, 1.05)]
+    for row in rows[:3]:
+        c = row[:3]
+        assert row[3] == c[0] * c[1] * c[2] + 1 and row[4] == gpu.tde_units(c)
+        cells = (24 // c[0]) * (30 // c[1]) * (30 // c[2])
+        assert row[8] == min(4.8828125 * 0.732 * min(1.0, cells / 64 ** 3), 4.8828125)
+        ref = oracle.RefHarness(specs, c, boundary=0)
+        h = gpu.Harness([gpu.AxisSpec(*s) for s in specs], c, HarnessOptions(boundary="outflow"))
+        init = report._ic(h)
+        h.set_state(init)
+        for r, f in enumerate(init):
+            ref.set_fields(r, f)
+        for _ in range(2):
+            ref.advance()
+        h.run(2)
+        assert row[5] == ref.ledger()[0] // 2
+        assert bits_equal(h.gather_interior(), ref.gather())
