@@ -2,10 +2,17 @@
 // reference build under oracle/_ref as the comparison).  The reference's
 // own RunConfig drives ppmlr::Harness on the CPU and GpuHarness on the GPU
 // side by side; every dt and the final interior must be bit-identical.
-//   usage: dropin_demo [steps] [px]
+//   usage: dropin_demo [steps] [px] [ndevices]
+// ndevices > 1 maps the blocks round-robin onto that many device slots
+// (ppmlr_gpu_harness_create_on); on a one-GPU box every slot is device 0,
+// which runs the same multi-device code path.
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+
+#include <cuda_runtime.h>
+
+#include <vector>
 
 #include "gpu_harness.hpp"
 #include "ppmlr/decomp.hpp"
@@ -22,7 +29,12 @@ int main(int argc, char** argv) {
     const StretchedGrid grid = cfg.make_grid();
     Harness cpu(grid, layout(cfg.partition, grid), cfg.make_options());
     cpu.init_magnetosphere(cfg.profiles);
-    GpuHarness gpu(cfg);
+    const int ndev = argc > 3 ? std::atoi(argv[3]) : 1;
+    int have = 1;
+    cudaGetDeviceCount(&have);
+    std::vector<int> devs;
+    for (int d = 0; d < ndev; ++d) devs.push_back(d % (have > 0 ? have : 1));
+    GpuHarness gpu(cfg, PPMLR_STRICT, devs);
     gpu.init_magnetosphere(cfg.profiles);
     for (long s = 0; s < steps; ++s) {
       const double a = cpu.advance(), b = gpu.advance();
@@ -36,8 +48,9 @@ int main(int argc, char** argv) {
       std::printf("state differs after %ld steps\n", steps);
       return 1;
     }
-    std::printf("drop-in OK: %ld steps, partition (%d,1,1), dt and %zu cells bit-identical\n",
-                steps, cfg.partition.nx, x.size());
+    std::printf("drop-in OK: %ld steps, partition (%d,1,1) on %d device slot(s), dt and %zu "
+                "cells bit-identical\n",
+                steps, cfg.partition.nx, ndev, x.size());
     return 0;
   } catch (const std::exception& e) {
     std::printf("error: %s\n", e.what());

@@ -27,7 +27,11 @@ inline void gpu_check(int rc) {
 
 class GpuHarness {
  public:
-  explicit GpuHarness(const RunConfig& cfg, int precision = PPMLR_STRICT, int device = 0) {
+  explicit GpuHarness(const RunConfig& cfg, int precision = PPMLR_STRICT, int device = 0)
+      : GpuHarness(cfg, precision, std::vector<int>{device}) {}
+  // One process driving several GPUs: block r on devices[r % size]
+  // (ppmlr_gpu_harness_create_on; e.g. {0,1,...,7} for the 8 GPUs of a box).
+  GpuHarness(const RunConfig& cfg, int precision, const std::vector<int>& devices) {
     ppmlr_axis_spec s[3];
     const AxisSpec* a[3] = {&cfg.grid_x, &cfg.grid_y, &cfg.grid_z};
     for (int i = 0; i < 3; ++i)
@@ -50,9 +54,10 @@ class GpuHarness {
     o.gamma = cfg.constants.gamma;
     o.pressure_floor = cfg.constants.pressure_floor;
     o.precision = precision;  // PPMLR_STRICT: bit-identical to the CPU build
-    o.device = device;
-    gpu_check(ppmlr_gpu_harness_create(s, cfg.partition.nx, cfg.partition.ny,
-                                       cfg.partition.nz, &o, &h_));
+    o.device = devices.empty() ? 0 : devices[0];
+    gpu_check(ppmlr_gpu_harness_create_on(s, cfg.partition.nx, cfg.partition.ny,
+                                          cfg.partition.nz, &o, devices.data(),
+                                          static_cast<int>(devices.size()), &h_));
     cells_ = static_cast<std::size_t>(cfg.grid_x.target_cells) * cfg.grid_y.target_cells *
              cfg.grid_z.target_cells;
   }

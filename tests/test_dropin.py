@@ -14,8 +14,9 @@ BIN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "dropin", "dropin
 
 @pytest.mark.gpu
 @pytest.mark.skipif(not os.path.exists(BIN), reason="dropin_demo not built")
-@pytest.mark.parametrize("px", [1, 2, 4])
-def test_cpp_dropin_bit_identical(gpu, px):
-    out = subprocess.run([BIN, "5", str(px)], capture_output=True, text=True, timeout=600)
+@pytest.mark.parametrize("px,ndev", [(1, 1), (2, 1), (4, 1), (4, 4), (8, 3)])
+def test_cpp_dropin_bit_identical(gpu, px, ndev):
+    out = subprocess.run([BIN, "5", str(px), str(ndev)], capture_output=True, text=True,
+                         timeout=600)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "drop-in OK" in out.stdout
