@@ -1,5 +1,5 @@
-// Persistent, prefetching schedule of the directional PPMLR sweep (fast
-// build, no dipole): the same per-pencil algorithm as sweep.cuh's
+// Persistent, prefetching schedule of the directional PPMLR sweep (both
+// builds, compile-time tile, with or without the dipole): the same per-pencil algorithm as sweep.cuh's
 // sweep_tile (proj/src/ppm1d.cpp:111-364, stepper.cpp:249-282) with three
 // changes of schedule, measured against the one-shot kernel on the B200:
 //
@@ -125,9 +125,12 @@ __device__ __forceinline__ bool sweep_tile_v2(const SweepArgs& A, const SweepMap
         auto win = [&](int j) { return pv[j * SS]; };
         auto dwin = [&](int j) { return dv[j * SS]; };
         zone_traced_dm(win, dwin, e0, e1, k, o, hs, tw, l, r);
-      } else {  // flat strip-end zone
+      } else if (Ops::kFastMath) {  // flat strip-end zone
         l = pv[0];
         r = pv[0];
+      } else {  // the reference's arithmetic on the flat parabola (-0 + 0 = +0)
+        l = avg_left(pv[0], pv[0], 0.0, hs, tw);
+        r = avg_right(pv[0], pv[0], 0.0, hs, tw);
       }
     };
     auto all8 = [&](auto F) {
@@ -309,7 +312,9 @@ __device__ __forceinline__ bool sweep_tile_v2(const SweepArgs& A, const SweepMap
         u[v] = LFT[v * T + ci] * scale + o.div(TR[v * T + ci] - TR[v * T + ci + SS], dxe, r_dxe);
     } else {
 #pragma unroll
-      for (int v = 0; v < 8; ++v) u[v] = LFT[v * T + ci] * scale;
+      for (int v = 0; v < 8; ++v)  // no sliver (strict: the reference's + (0 - 0)/dx)
+        u[v] = Ops::kFastMath ? LFT[v * T + ci] * scale
+                              : LFT[v * T + ci] * scale + o.div(0.0 - 0.0, dxe, r_dxe);
     }
     cs[0] = u[kRho];
     cs[1 + a] = u[kUn];

@@ -132,3 +132,34 @@ def test_bench_workload_c5_magnetosphere_fast_vs_strict(gpu):
     print("mag1024 rel L1", l1.max(), "rel Linf", linf.max(), "rel time", rel_t)
     assert np.all(l1 <= FAST_L1) and np.all(linf <= FAST_LINF), (l1, linf)
     assert rel_t <= 1e-12
+
+
+@pytest.mark.parametrize("dims,dipole", [((300, 20, 12), False), ((20, 260, 14), False),
+                                         ((18, 12, 290), False), ((264, 36, 20), True)])
+def test_fast_partial_compile_time_tiles_within_tolerance(gpu, dims, dipole):
+    """Axes >= 256 cells that are not a multiple of 64 take the compile-time
+    tile with a partial last segment (and partial pencil groups on the
+    short axes): the persistent fast kernel (sweep_v2.cuh) against the
+    strict one-shot kernel, 8 steps, blast physics / the magnetosphere."""
+    from paper_1607_02214_b200.api import AxisSpec, HarnessOptions
+    out = {}
+    for prec in ("strict", "fast"):
+        if dipole:
+            specs = [AxisSpec(-48.0, -48.0 + 1.2 * dims[0], -48.0, -48.0 + 1.2 * dims[0], 1.2,
+                              dims[0], 1.05)] + [
+                AxisSpec(-0.6 * n * 1.0, 0.6 * n, -0.6 * n, 0.6 * n, 1.2, n, 1.05)
+                for n in dims[1:]]
+            opts = HarnessOptions(boundary=gpu.MAGNETOSPHERE, with_dipole=True, precision=prec)
+        else:
+            specs = [AxisSpec(-1.0, 1.0, -1.0, 1.0, 2.0 / n, n, 1.05) for n in dims]
+            opts = HarnessOptions(precision=prec)
+        h = gpu.Harness(specs, (1, 1, 1), opts)
+        if dipole:
+            h.init_magnetosphere()
+        else:
+            h.init_with(gpu.IC_BLAST, (10.0, 0.1, 0.4))
+        h.run(8)
+        out[prec] = h.gather_interior()
+        h.close()
+    l1, linf = rel_errors(out["fast"], out["strict"])
+    assert np.all(l1 <= FAST_L1) and np.all(linf <= FAST_LINF), (l1, linf)
