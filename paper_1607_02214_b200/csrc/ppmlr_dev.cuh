@@ -90,10 +90,18 @@ template <class Ops>
 __device__ __forceinline__ void fast_speed3_all(const double* s, double bdx, double bdy,
                                                 double bdz, const KC& k, Ops& o, double* cf) {
   const double b0 = s[4] + bdx, b1 = s[5] + bdy, b2 = s[6] + bdz;
-  const double mr = k.c.mu0 * s[0];
-  const double r_mr = o.rcp(mr);
-  const double a2 = o.dv(k.c.gamma * s[7], s[0]);
-  const double ca2 = o.div((b0 * b0 + b1 * b1) + b2 * b2, mr, r_mr);
+  double a2, ca2, r_mr, mr = 0.0;
+  if constexpr (Ops::kFastMath && PPMLR_FAST_RCP_SHARE) {
+    const double r_rho = o.rcp(s[0]);
+    r_mr = k.r_mu0 * r_rho;
+    a2 = (k.c.gamma * s[7]) * r_rho;
+    ca2 = ((b0 * b0 + b1 * b1) + b2 * b2) * r_mr;
+  } else {
+    mr = k.c.mu0 * s[0];
+    r_mr = o.rcp(mr);
+    a2 = o.dv(k.c.gamma * s[7], s[0]);
+    ca2 = o.div((b0 * b0 + b1 * b1) + b2 * b2, mr, r_mr);
+  }
   const double sum = a2 + ca2;
   const double ss = sum * sum;
   const double a4 = 4.0 * a2;
