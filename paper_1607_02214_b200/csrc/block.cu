@@ -461,7 +461,8 @@ void choose_sweep_tiles(ppmlr_gpu_block* b) {
   for (int a = 0; a < 3; ++a) {
     const int n = b->n[a];
     int L;
-    if (env_int("PPMLR_SWEEP_RUNTIME_TL", 0) == 0 && (n % Lc == 0 || n >= 4 * Lc)) {
+    if (env_int("PPMLR_SWEEP_RUNTIME_TL", 0) == 0 &&
+        (n % Lc == 0 || n >= 4 * Lc || env_int("PPMLR_SWEEP_FORCE_CT", 0))) {
       L = Lc;
     } else {
       const int nseg = (n + Lmax - 1) / Lmax;

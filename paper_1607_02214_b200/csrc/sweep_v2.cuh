@@ -38,8 +38,10 @@ __device__ __forceinline__ bool sweep_tile_v2(const SweepArgs& A, const SweepMap
                                               const TileId id, double* smem, double* FLD,
                                               unsigned long long* s_err, bool& stored) {
   bool tbad = false;
-  constexpr int NT = NP * TL;
-  constexpr int T = slot_stride(NT);
+  // TL > 0: the compile-time tile; TL == 0: the block's runtime tile L + 8
+  const int TLr = TL > 0 ? TL : A.L + 8;
+  const int NT = NP * TLr;
+  const int T = slot_stride(NT);
   double* TR = smem + 16 * T;
   double* LFT = smem + 24 * T;
   double* CF = smem + 32 * T;
@@ -47,20 +49,20 @@ __device__ __forceinline__ bool sweep_tile_v2(const SweepArgs& A, const SweepMap
   const int seg = id.seg, grp = id.grp, oc = id.oc;
   const int nn = A.n + 8;
   const int seg0 = seg * A.L;
-  const int TLv = min(TL, nn - seg0);
+  const int TLv = min(TLr, nn - seg0);
   const bool final_seg = seg == A.nseg - 1;
-  const int zmax = final_seg ? TLv - 2 : TL - 3;
+  const int zmax = final_seg ? TLv - 2 : TLr - 3;
   const int g0 = grp * NP;
   const int npv = min(NP, A.ng - g0);
-  const bool whole = TLv == TL && npv == NP;
+  const bool whole = TLv == TLr && npv == NP;
   const double dt = *A.dt;
   const Consts& c = A.c;
   const KC k = make_kc(c);
   const int ci = threadIdx.x;
   int s, p;
   if (AXIS == 0) {
-    p = ci / TL;
-    s = ci - p * TL;
+    p = ci / TLr;
+    s = ci - p * TLr;
   } else {
     s = ci / NP;
     p = ci - s * NP;
@@ -352,8 +354,9 @@ template <int AXIS, int NP, int TL>
 __device__ __forceinline__ void tma_load_fields(const SweepArgs& A, const SweepMaps& M,
                                                 const TileId id, double* FLD,
                                                 unsigned long long* mbar) {
-  constexpr int T = slot_stride(NP * TL);
-  constexpr unsigned kBox = NP * TL * sizeof(double);
+  const int TLr = TL > 0 ? TL : A.L + 8;
+  const int T = slot_stride(NP * TLr);
+  const unsigned kBox = NP * TLr * sizeof(double);
   const int a0 = id.seg * A.L, g = id.grp * NP + 4, o = id.oc + 4;
   const int cx = AXIS == 0 ? a0 : g;
   const int cy = AXIS == 0 ? g : (AXIS == 1 ? a0 : o);
@@ -396,7 +399,7 @@ __device__ __forceinline__ TileId tile_of_v2(const SweepArgs& A, int t) {
 // counter, so tiles with a moving edge — dearer — balance across CTAs)
 // when the current one starts and prefetches its fields.
 template <int AXIS, bool DIPOLE, int NP, int TL>
-__global__ void __launch_bounds__(NP * TL, PPMLR_SWEEP_V2_MINB)
+__global__ void __launch_bounds__(NP*(TL > 0 ? TL : kSweepTL), PPMLR_SWEEP_V2_MINB)
     sweep_kernel_v2(const SweepArgs A, const __grid_constant__ SweepMaps M) {
   extern __shared__ __align__(128) double smem[];
   __shared__ unsigned long long s_err;
@@ -404,7 +407,7 @@ __global__ void __launch_bounds__(NP * TL, PPMLR_SWEEP_V2_MINB)
   // the claimed tile of each buffer, decoded once by the elected thread:
   // {t, seg, grp, oc}
   __shared__ int s_tile[2][4];
-  constexpr int T = slot_stride(NP * TL);
+  const int T = slot_stride(NP * (TL > 0 ? TL : A.L + 8));
   const int ntiles = (AXIS == 0 ? split_count(A.part, A.cl, A.cr, A.nseg) : A.nseg) *
                      (AXIS == 0 ? A.ngroups : split_count(A.part, A.cl, A.cr, A.ngroups)) * A.no;
   auto claim = [&](int slot, int t) {  // elected thread
