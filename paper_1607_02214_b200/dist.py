@@ -161,7 +161,6 @@ class Exchanger:
         self.finish(blk, faces, layers)
 
     def allreduce_min(self, t):
-        import torch
         import torch.distributed as dist
         if self.transport == "nccl" or t.device.type == "cpu":
             dist.all_reduce(t, op=dist.ReduceOp.MIN, group=self.group)
@@ -169,7 +168,6 @@ class Exchanger:
             h = t.cpu()
             dist.all_reduce(h, op=dist.ReduceOp.MIN, group=self.group)
             t.copy_(h)
-        del torch
 
     def halo_ms(self):
         """Summed NCCL halo time of the timed exchanges (comm stream events)."""

@@ -8,7 +8,6 @@ report the reference's first failure (rank order within the earliest
 phase)."""
 from __future__ import annotations
 
-import numpy as np
 import pytest
 
 from conftest import bits_equal
