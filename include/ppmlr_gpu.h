@@ -208,6 +208,11 @@ int ppmlr_gpu_block_synchronize(ppmlr_gpu_block* b);
  * ghost width (4).  For on-device consumers (analysis, comparisons). */
 int ppmlr_gpu_block_state_view(ppmlr_gpu_block* b, double** field_planes, long long* strides,
                                int* dims);
+/* init_with of a built-in IC (kinds 0..3, see ppmlr_gpu_harness_init_ic)
+ * evaluated on the device for this block (and its dipole, when it has one):
+ * no host arrays, bit-identical to the host evaluation.  Clears the frozen
+ * core. */
+int ppmlr_gpu_block_init_ic(ppmlr_gpu_block* b, int kind, const double* params);
 /* The dipole field B_d (3 planes, same layout as the state) or NULLs;
  * returns 1 when the block carries one. */
 int ppmlr_gpu_block_dipole_view(ppmlr_gpu_block* b, double** bd_planes);

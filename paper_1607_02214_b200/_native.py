@@ -145,6 +145,7 @@ _sig("ppmlr_gpu_block_synchronize", C.c_int, _BP)
 _sig("ppmlr_gpu_block_state_view", C.c_int, _BP, C.POINTER(C.c_void_p),
      C.POINTER(C.c_longlong), C.POINTER(C.c_int))
 _sig("ppmlr_gpu_block_dipole_view", C.c_int, _BP, C.POINTER(C.c_void_p))
+_sig("ppmlr_gpu_block_init_ic", C.c_int, _BP, C.c_int, C.POINTER(C.c_double))
 _sig("ppmlr_gpu_block_check", C.c_int, _BP)
 _sig("ppmlr_gpu_block_timing", C.c_int, _BP, C.c_int, _dp, _dp, C.POINTER(C.c_long))
 _sig("ppmlr_gpu_sweep_strips", C.c_int, _dp, _dp, _dp, C.c_int, C.c_int, C.c_int, C.c_int,

@@ -440,6 +440,25 @@ def host_block_state(specs, partition=(1, 1, 1), options: HarnessOptions | None 
                 spacings=[cat_s[offs[a]:offs[a + 1]] for a in range(3)])
 
 
+def host_block_geometry(specs, partition=(1, 1, 1), options: HarnessOptions | None = None,
+                        rank=0):
+    """Ghost-inclusive centres and spacings of block `rank` (make_block's
+    local axes), without evaluating any state."""
+    options = options or HarnessOptions()
+    blocks, _ = layout(specs, partition)
+    info = blocks[rank]
+    g = options.ghost
+    spans = [info.n[a] + 2 * g for a in range(3)]
+    cat_c, cat_s = np.zeros(sum(spans)), np.zeros(sum(spans))
+    p = np.zeros(8)
+    check(N.lib.ppmlr_host_block_state(_specs3(specs), *partition, C.byref(options.c()), rank,
+                                       0, ptr(p), None, None, None, None, None,
+                                       ptr(cat_c), ptr(cat_s)))
+    offs = np.cumsum([0] + spans)
+    return ([cat_c[offs[a]:offs[a + 1]] for a in range(3)],
+            [cat_s[offs[a]:offs[a + 1]] for a in range(3)])
+
+
 def device_count():
     return int(N.lib.ppmlr_gpu_device_count())
 

@@ -1823,6 +1823,17 @@ int ppmlr_gpu_block_state_view(ppmlr_gpu_block* b, double** field_planes, long l
   return kG;
 }
 
+int ppmlr_gpu_block_init_ic(ppmlr_gpu_block* b, int kind, const double* params) {
+  if (!device_init_supported(kind) || kind < 0) {
+    set_error("block_init_ic: kind must be 0..3 (device-evaluated ICs)");
+    return PPMLR_INVALID_SPEC;
+  }
+  if (int rc = block_set_frozen(b, nullptr, nullptr, 0)) return rc;
+  double p[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (params) std::memcpy(p, params, sizeof p);
+  return block_init_device(b, kind, p, true);
+}
+
 int ppmlr_gpu_block_dipole_view(ppmlr_gpu_block* b, double** bd_planes) {
   for (int a = 0; a < 3; ++a) bd_planes[a] = b->bd ? b->bd + (long long)a * b->ncell : nullptr;
   return b->bd ? 1 : 0;

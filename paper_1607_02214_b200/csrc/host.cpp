@@ -890,7 +890,9 @@ int ppmlr_host_block_state(const ppmlr_axis_spec specs[3], int px, int py, int p
       ci.kind = ic_kind;
       ci.ic = ic_of(ic_kind, params);
     }
-    block_fill(hb, ci, f, opts->with_dipole ? &bdv : nullptr);
+    // geometry only (no state requested): skip the fill
+    if (fields || bd || frozen_idx || frozen_states || n_frozen)
+      block_fill(hb, ci, f, opts->with_dipole ? &bdv : nullptr);
     if (fields) std::copy(f.begin(), f.end(), fields);
     if (bd && !bdv.empty()) std::copy(bdv.begin(), bdv.end(), bd);
     if (frozen_idx) std::copy(fidx.begin(), fidx.end(), frozen_idx);

@@ -237,15 +237,24 @@ class DeviceRankBlock:
     def __init__(self, specs, partition, options, rank, ic, device):
         import torch
         from . import _native as N
-        from .api import _BOUNDARY, _PRECISION, check, host_block_state, layout
+        from .api import (_BOUNDARY, _PRECISION, check, host_block_geometry, host_block_state,
+                          layout)
         self.N = N
         self.check_rc = check
         blocks, _ = layout(specs, partition)
         self.info = blocks[rank]
-        st = host_block_state(specs, partition, options, rank, ic)
+        # built-in ICs are evaluated on the device (no host copy of the
+        # block); init_magnetosphere is streamed from the host
+        on_device = ic[0] != "magnetosphere" and 0 <= int(ic[0]) <= 3
+        if on_device:
+            cen, spc = host_block_geometry(specs, partition, options, rank)
+            st = None
+        else:
+            st = host_block_state(specs, partition, options, rank, ic)
+            cen, spc = st["centers"], st["spacings"]
         d = N.BlockDesc()
         g = options.ghost
-        self._geom = [np.ascontiguousarray(x) for x in st["centers"] + st["spacings"]]
+        self._geom = [np.ascontiguousarray(x) for x in list(cen) + list(spc)]
         for a in range(3):
             d.n[a] = self.info.n[a]
             d.lo[a] = self.info.lo[a]
@@ -268,7 +277,13 @@ class DeviceRankBlock:
         self.device = device
         self.stream = torch.cuda.current_stream(device)
         check(N.lib.ppmlr_gpu_block_set_stream(h, C.c_void_p(self.stream.cuda_stream)))
-        self.upload(st["fields"], st["bd"], st["frozen_idx"], st["frozen_states"])
+        if on_device:
+            p = np.zeros(8)
+            p[:len(ic[1])] = ic[1]
+            check(N.lib.ppmlr_gpu_block_init_ic(h, int(ic[0]),
+                                                p.ctypes.data_as(C.POINTER(C.c_double))))
+        else:
+            self.upload(st["fields"], st["bd"], st["frozen_idx"], st["frozen_states"])
         self._dt = torch.as_tensor(_CudaPtr(N.lib.ppmlr_gpu_block_dt_slot(h), 1),
                                    device=f"cuda:{device}")
         self.n = self.info.n
