@@ -403,18 +403,20 @@ class Harness:
 
 
 def host_block_state(specs, partition=(1, 1, 1), options: HarnessOptions | None = None,
-                     rank=0, ic=("magnetosphere",)):
+                     rank=0, ic=("magnetosphere",), fields_out=None):
     """Host-side (no GPU) initial state of block `rank` as the Harness builds
     and uploads it.  ic = ("magnetosphere", [rho_core, p_core, falloff, r_ref])
     or (kind, params).  Returns dict(fields, bd, frozen_idx, frozen_states,
-    centers, spacings); arrays ghost-inclusive, reference index order."""
+    centers, spacings); arrays ghost-inclusive, reference index order.
+    fields_out: a caller array (e.g. pinned) of that shape to fill in place."""
     options = options or HarnessOptions()
     blocks, _ = layout(specs, partition)
     info = blocks[rank]
     g = options.ghost
     spans = [info.n[a] + 2 * g for a in range(3)]
     cells = spans[0] * spans[1] * spans[2]
-    fields = np.zeros((spans[2], spans[1], spans[0], 8))
+    fields = fields_out if fields_out is not None else np.zeros((spans[2], spans[1], spans[0], 8))
+    assert fields.shape == (spans[2], spans[1], spans[0], 8) and fields.dtype == np.float64
     bd = np.zeros((spans[2], spans[1], spans[0], 3)) if options.with_dipole else None
     if ic[0] == "magnetosphere":
         kind = -1
@@ -423,7 +425,7 @@ def host_block_state(specs, partition=(1, 1, 1), options: HarnessOptions | None 
         kind = int(ic[0])
         p = np.zeros(8)
         p[:len(ic[1])] = ic[1]
-    fidx = np.zeros(cells, np.int64)
+    fidx = np.zeros(cells if kind < 0 else 1, np.int64)  # frozen cells: magnetosphere only
     fst = np.zeros((cells, 8)) if kind < 0 else np.zeros((1, 8))
     nf = C.c_int64()
     cat_c, cat_s = np.zeros(sum(spans)), np.zeros(sum(spans))

@@ -890,11 +890,14 @@ int ppmlr_host_block_state(const ppmlr_axis_spec specs[3], int px, int py, int p
       ci.kind = ic_kind;
       ci.ic = ic_of(ic_kind, params);
     }
-    // geometry only (no state requested): skip the fill
-    if (fields || bd || frozen_idx || frozen_states || n_frozen)
+    // straight into the caller's arrays (every cell's 8 values, and its
+    // dipole, are written); geometry only when no state is requested
+    if (fields) {
+      ci(0, hb.n[2] + 2 * hb.g, fields, opts->with_dipole ? bd : nullptr);
+    } else if (bd || frozen_idx || frozen_states || n_frozen) {
       block_fill(hb, ci, f, opts->with_dipole ? &bdv : nullptr);
-    if (fields) std::copy(f.begin(), f.end(), fields);
-    if (bd && !bdv.empty()) std::copy(bdv.begin(), bdv.end(), bd);
+      if (bd && !bdv.empty()) std::copy(bdv.begin(), bdv.end(), bd);
+    }
     if (frozen_idx) std::copy(fidx.begin(), fidx.end(), frozen_idx);
     if (frozen_states) std::copy(fst.begin(), fst.end(), frozen_states);
     if (n_frozen) *n_frozen = (int64_t)fidx.size();

@@ -400,9 +400,11 @@ def _e2e_distributed(blk, ex, cfg, rank, world, args, cfl, srcs, cells_rank, loc
     import torch
     import torch.distributed as dist
     from .api import host_block_state
-    st = host_block_state(cfg.specs, cfg.partition, cfg.options, rank, cfg.ic)
-    fin = torch.empty(st["fields"].shape, dtype=torch.float64, pin_memory=True).numpy()
-    fin[...] = st["fields"]
+    g = cfg.options.ghost
+    shape = tuple(blk.n[2 - a] + 2 * g for a in range(3)) + (8,)
+    fin = torch.empty(shape, dtype=torch.float64, pin_memory=True).numpy()
+    # the rank's initial state evaluated straight into the pinned buffer
+    st = host_block_state(cfg.specs, cfg.partition, cfg.options, rank, cfg.ic, fields_out=fin)
     nx, ny, nz = blk.n
     fout = torch.empty((nz, ny, nx, 8), dtype=torch.float64, pin_memory=True).numpy()
     k = args.steps
