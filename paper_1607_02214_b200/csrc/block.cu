@@ -148,8 +148,15 @@ __global__ void soa_to_interior_kernel(double* __restrict__ out, Planes src, Lay
 // apply_boundaries (stepper.cpp:202-247) for one axis, `layers` ghost layers,
 // over the interior transverse span.  mode: 0 outflow, 1 periodic,
 // 2 magnetosphere (the sunward +x shell is constant and pre-filled).
-__global__ void bc_kernel(Planes s, Lay L, int axis, int phys_lo, int phys_hi, int layers,
-                          int mode) {
+// One launch fills the faces of every axis in `axes` (packed 2 bits per
+// entry, blockIdx.y selects the entry): the slabs of different axes are
+// disjoint (interior transverse ranges only).
+struct BcAxes {
+  int axis[3], lo[3], hi[3];
+};
+
+__global__ void bc_kernel(Planes s, Lay L, BcAxes ax, int layers, int mode) {
+  const int axis = ax.axis[blockIdx.y], phys_lo = ax.lo[blockIdx.y], phys_hi = ax.hi[blockIdx.y];
   const int na = axis == 0 ? L.n0 : (axis == 1 ? L.n1 : L.n2);
   const int nb = axis == 0 ? L.n1 : (axis == 1 ? L.n2 : L.n0);
   const int nc = axis == 0 ? L.n2 : (axis == 1 ? L.n0 : L.n1);
@@ -559,14 +566,21 @@ int launch_sweep(ppmlr_gpu_block* b, int axis, int phase, int part) {
 int launch_bc(ppmlr_gpu_block* b, int axis_mask, int layers) {
   const Lay L = lay_of(b);
   Planes s = planes(cur_buf(b), b->ncell);
+  BcAxes ax{};
+  int na = 0;
+  long long work = 0;
   for (int a = 0; a < 3; ++a) {
     if (!(axis_mask & (1 << a))) continue;
     if (!b->physical[a][0] && !b->physical[a][1]) continue;
-    const long long work = 2LL * layers * b->n[(a + 1) % 3] * b->n[(a + 2) % 3];
-    bc_kernel<<<grid_for(work), 256, 0, b->stream>>>(s, L, a, b->physical[a][0],
-                                                      b->physical[a][1], layers, b->boundary);
-    b->kernel_launches += 1;
+    ax.axis[na] = a;
+    ax.lo[na] = b->physical[a][0];
+    ax.hi[na] = b->physical[a][1];
+    ++na;
+    work = std::max(work, 2LL * layers * b->n[(a + 1) % 3] * b->n[(a + 2) % 3]);
   }
+  if (na == 0) return 0;
+  bc_kernel<<<dim3(grid_for(work), na), 256, 0, b->stream>>>(s, L, ax, layers, b->boundary);
+  b->kernel_launches += 1;
   CK(cudaGetLastError());
   return 0;
 }
