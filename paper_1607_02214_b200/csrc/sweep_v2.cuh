@@ -33,10 +33,23 @@
 namespace ppmlr_b200 {
 namespace PPMLR_KNS {
 
-template <int AXIS, bool DIPOLE, int NP, int TL, class Ops>
+#ifndef PPMLR_SWEEP_V2_RSMEM
+// The traced right states go through the idle FLD buffer (the next tile's
+// fields are requested after P4 instead of at the tile start: the load still
+// has most of the tile to land) instead of being held in registers across
+// P3's barrier.
+#ifdef PPMLR_FAST_MATH
+#define PPMLR_SWEEP_V2_RSMEM 1  // measured: fast blast -0.4%, C5 -1.2%, C2 -1.6% sweep time
+#else
+#define PPMLR_SWEEP_V2_RSMEM 0  // strict: +2.9% on the blast (kept in registers)
+#endif
+#endif
+
+template <int AXIS, bool DIPOLE, int NP, int TL, class Ops, class Prefetch>
 __device__ __forceinline__ bool sweep_tile_v2(const SweepArgs& A, const SweepMaps& M,
                                               const TileId id, double* smem, double* FLD,
-                                              unsigned long long* s_err, bool& stored) {
+                                              double* RSB, unsigned long long* s_err,
+                                              bool& stored, const Prefetch& prefetch) {
   bool tbad = false;
   // TL > 0: the compile-time tile; TL == 0: the block's runtime tile L + 8
   const int TLr = TL > 0 ? TL : A.L + 8;
@@ -155,6 +168,10 @@ __device__ __forceinline__ bool sweep_tile_v2(const SweepArgs& A, const SweepMap
           if (badR) R[v] = own;
         }
       }
+      if (PPMLR_SWEEP_V2_RSMEM) {
+#pragma unroll
+        for (int v = 0; v < 8; ++v) RSB[v * T + ci] = R[v];
+      }
     };
     if (flat)
       all8(FlatTag<true>{});
@@ -182,7 +199,13 @@ __device__ __forceinline__ bool sweep_tile_v2(const SweepArgs& A, const SweepMap
     }
     const SmemVec qr{LFT + ci + SS, T};
     Ops o;
-    const double us = solve_edge<double[8], SmemVec, Ops, DIPOLE>(R, qr, bl, br, k, f, o);
+    double us;
+    if (PPMLR_SWEEP_V2_RSMEM) {
+      const SmemVec ql{RSB + ci, T};
+      us = solve_edge<SmemVec, SmemVec, Ops, DIPOLE>(ql, qr, bl, br, k, f, o);
+    } else {
+      us = solve_edge<double[8], SmemVec, Ops, DIPOLE>(R, qr, bl, br, k, f, o);
+    }
     tbad |= o.bad;
     CF[ci + SS] = us;
     mv = s + 1 >= 4 && s + 1 <= TLv - 4 && us * dt != 0.0;
@@ -190,6 +213,7 @@ __device__ __forceinline__ bool sweep_tile_v2(const SweepArgs& A, const SweepMap
     for (int v = 0; v < 8; ++v) TR[v * T + ci + SS] = f[v];
   }
   const bool moving = __syncthreads_or(mv);
+  if (PPMLR_SWEEP_V2_RSMEM) prefetch();  // the right states in RSB are consumed
 
   // ---- P7: Lagrangian update of zones [3, zmax-1] -> LFT -------------------
   // (moving tiles: every cell's conserved state -> FLD for the remap)
@@ -435,22 +459,28 @@ __global__ void __launch_bounds__(NP*(TL > 0 ? TL : kSweepTL), PPMLR_SWEEP_V2_MI
     if (t >= ntiles) break;
     double* FLD = smem + buf * 8 * T;
     const TileId id = {s_tile[buf][1], s_tile[buf][2], s_tile[buf][3]};
+    double* NXT = smem + (buf ^ 1) * 8 * T;
+    int tn = 0;
+    TileId idn{0, 0, 0};
     if (threadIdx.x == 0) {
-      const int tn = PPMLR_SWEEP_V2_DYN ? (int)gridDim.x + (int)atomicAdd(A.tile_ctr, 1u)
-                                        : t + (int)gridDim.x;
-      const TileId idn = claim(buf ^ 1, tn);
-      if (tn < ntiles) {
-        // the other buffer held the previous tile's result box: its TMA
-        // store must have read it before the next tile's fields land there
-        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        tma_load_fields<AXIS, NP, TL>(A, M, idn, smem + (buf ^ 1) * 8 * T, &s_mbar[buf ^ 1]);
-      }
+      tn = PPMLR_SWEEP_V2_DYN ? (int)gridDim.x + (int)atomicAdd(A.tile_ctr, 1u)
+                              : t + (int)gridDim.x;
+      idn = claim(buf ^ 1, tn);
+      // the other buffer held the previous tile's result box: its TMA store
+      // must have read it before it is reused (scratch, then the next fields)
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
     }
+    auto prefetch = [&]() {
+      if (threadIdx.x == 0 && tn < ntiles) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        tma_load_fields<AXIS, NP, TL>(A, M, idn, NXT, &s_mbar[buf ^ 1]);
+      }
+    };
+    if (!PPMLR_SWEEP_V2_RSMEM) prefetch();
     mbar_wait(&s_mbar[buf], (unsigned)(i >> 1) & 1u);
     bool stored = false;
-    const bool bad =
-        sweep_tile_v2<AXIS, DIPOLE, NP, TL, MainOps>(A, M, id, smem, FLD, &s_err, stored);
+    const bool bad = sweep_tile_v2<AXIS, DIPOLE, NP, TL, MainOps>(A, M, id, smem, FLD, NXT,
+                                                                  &s_err, stored, prefetch);
     const bool any_bad = __syncthreads_or(bad);
     if (threadIdx.x == 0) {
       if (stored) {
