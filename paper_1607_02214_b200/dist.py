@@ -217,8 +217,8 @@ def advance(blk, ex, step, cfl, with_sources, group=None, overlap=True):
             need = ((2 * nxt, 2 * nxt + 1), 4)
         elif with_sources:
             need = (tuple(range(6)), 1)
-        else:
-            need = (((0, 1) if next_first_x else ()), 4)
+        else:  # the frozen-core restore still changes the state: exchange after it
+            need = ((), 4)
         _produce(blk, ex, lambda part, a=axis, s=k: blk.sweep_part(a, s, part), need[0],
                  need[1], overlap)
     if with_sources:
@@ -228,6 +228,8 @@ def advance(blk, ex, step, cfl, with_sources, group=None, overlap=True):
                  (0, 1) if next_first_x else (), 4, overlap)
     else:
         blk.end_step(cfl, False)
+        if next_first_x:
+            ex.start(blk, (0, 1), 4)
     ex.allreduce_min(blk.dt_tensor())
 
 

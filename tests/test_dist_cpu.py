@@ -140,10 +140,13 @@ def _cfg(configs, name):
         return configs.magnetosphere_small(n=(32, 18, 18), dcell=2.4)
     if name == "blast":
         return configs.blast(n=16, gpus=2, radius=0.3)
+    if name == "blast_nosources":
+        return configs.blast(n=16, gpus=2, radius=0.3, with_sources=False)
     raise ValueError(name)
 
 
 @pytest.mark.parametrize("cfg_name,partition,steps", [("blast", (2, 1, 1), 4),
+                                                      ("blast_nosources", (2, 1, 1), 3),
                                                       ("magnetosphere_small", (2, 1, 1), 3)])
 def test_distributed_schedule_matches_single_block(tmp_path, oracle, cfg_name, partition,
                                                    steps):
