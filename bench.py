@@ -421,18 +421,25 @@ def bench_e2e(h, cfg, args, cells):
     h.advance()
     blk.download_interior(out=host_out)
     torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    blk.upload(host_in, st["bd"], st["frozen_idx"], st["frozen_states"])
-    for _ in range(k):
-        h.advance()
-    blk.download_interior(out=host_out)
-    t1 = time.perf_counter()
+    # wall clock is exposed to host jitter: short passes (< 1 s) are timed
+    # three times and the best is kept
+    best = None
+    for _ in range(3):
+        t0 = time.perf_counter()
+        blk.upload(host_in, st["bd"], st["frozen_idx"], st["frozen_states"])
+        for _ in range(k):
+            h.advance()
+        blk.download_interior(out=host_out)
+        t1 = time.perf_counter()
+        best = t1 - t0 if best is None else min(best, t1 - t0)
+        if t1 - t0 >= 1.0:
+            break
     h2d = host_in.nbytes + (st["bd"].nbytes if st["bd"] is not None else 0)
     d2h = host_out.nbytes + 8 * k
-    return {"value": cells * k / (t1 - t0), "unit": UNIT,
+    return {"value": cells * k / best, "unit": UNIT,
             "h2d_bytes_per_step": h2d / k, "d2h_bytes_per_step": d2h / k,
             "how": f"upload(pinned) + {k} x advance() + download_interior(pinned), wall "
-                   "clock, after one untimed pass"}
+                   "clock, after one untimed pass; best of 3 passes when a pass is < 1 s"}
 
 
 def bench_reference(args):
