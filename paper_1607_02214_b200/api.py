@@ -403,12 +403,13 @@ class Harness:
 
 
 def host_block_state(specs, partition=(1, 1, 1), options: HarnessOptions | None = None,
-                     rank=0, ic=("magnetosphere",), fields_out=None):
+                     rank=0, ic=("magnetosphere",), fields_out=None, bd_out=None):
     """Host-side (no GPU) initial state of block `rank` as the Harness builds
     and uploads it.  ic = ("magnetosphere", [rho_core, p_core, falloff, r_ref])
     or (kind, params).  Returns dict(fields, bd, frozen_idx, frozen_states,
     centers, spacings); arrays ghost-inclusive, reference index order.
-    fields_out: a caller array (e.g. pinned) of that shape to fill in place."""
+    fields_out / bd_out: caller arrays (e.g. pinned) of those shapes to fill
+    in place."""
     options = options or HarnessOptions()
     blocks, _ = layout(specs, partition)
     info = blocks[rank]
@@ -417,7 +418,9 @@ def host_block_state(specs, partition=(1, 1, 1), options: HarnessOptions | None 
     cells = spans[0] * spans[1] * spans[2]
     fields = fields_out if fields_out is not None else np.zeros((spans[2], spans[1], spans[0], 8))
     assert fields.shape == (spans[2], spans[1], spans[0], 8) and fields.dtype == np.float64
-    bd = np.zeros((spans[2], spans[1], spans[0], 3)) if options.with_dipole else None
+    bd = None
+    if options.with_dipole:
+        bd = bd_out if bd_out is not None else np.zeros((spans[2], spans[1], spans[0], 3))
     if ic[0] == "magnetosphere":
         kind = -1
         p = np.array(list(ic[1]) if len(ic) > 1 else [1.0, 0.1, 3.0, 3.0], dtype=np.float64)

@@ -405,8 +405,12 @@ def _e2e_distributed(blk, ex, cfg, rank, world, args, cfl, srcs, cells_rank, loc
     g = cfg.options.ghost
     shape = tuple(blk.n[2 - a] + 2 * g for a in range(3)) + (8,)
     fin = torch.empty(shape, dtype=torch.float64, pin_memory=True).numpy()
-    # the rank's initial state evaluated straight into the pinned buffer
-    st = host_block_state(cfg.specs, cfg.partition, cfg.options, rank, cfg.ic, fields_out=fin)
+    bdin = None
+    if cfg.options.with_dipole:
+        bdin = torch.empty(shape[:3] + (3,), dtype=torch.float64, pin_memory=True).numpy()
+    # the rank's initial state evaluated straight into the pinned buffers
+    st = host_block_state(cfg.specs, cfg.partition, cfg.options, rank, cfg.ic, fields_out=fin,
+                          bd_out=bdin)
     nx, ny, nz = blk.n
     fout = torch.empty((nz, ny, nx, 8), dtype=torch.float64, pin_memory=True).numpy()
     k = args.steps
