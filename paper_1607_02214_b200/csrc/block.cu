@@ -978,6 +978,7 @@ void ppmlr_gpu_block_destroy(ppmlr_gpu_block* b) {
   if (b->snap_stream) cudaStreamSynchronize(b->snap_stream);
   cudaFree(b->d_snap);
   if (b->snap_stream) cudaStreamDestroy(b->snap_stream);
+  if (b->copy_stream) cudaStreamDestroy(b->copy_stream);
   if (b->snap_ready) cudaEventDestroy(b->snap_ready);
   cudaFree(b->fslot);
   cudaFree(b->fstates);
@@ -991,6 +992,11 @@ void ppmlr_gpu_block_destroy(ppmlr_gpu_block* b) {
   for (auto ev : b->timing.pool) cudaEventDestroy(ev);
   if (b->stream && b->own_stream) cudaStreamDestroy(b->stream);
   delete b;
+}
+
+static int ensure_copy_stream(ppmlr_gpu_block* b) {
+  if (!b->copy_stream) CK(cudaStreamCreateWithFlags(&b->copy_stream, cudaStreamNonBlocking));
+  return 0;
 }
 
 static int ensure_scratch(ppmlr_gpu_block* b, size_t bytes) {
@@ -1098,55 +1104,67 @@ int block_upload_streamed(ppmlr_gpu_block* b, const ChunkFill& fill, bool with_b
   // src_fields given: copy straight from the caller's buffers (pinned
   // memory DMAs at full PCIe rate); otherwise fill pinned staging chunks
   const bool direct = src_fields != nullptr;
+  if (int rc = ensure_copy_stream(b)) return rc;
+  // chunk copies on the copy stream, conversion kernels on the block stream:
+  // the copy of chunk q+1 overlaps the kernels of chunk q (cdone: copy into
+  // scratch q finished; kdone: kernels done with scratch q)
   struct Staging {  // released on every exit path (CK returns, a throwing fill)
-    cudaStream_t st;
+    cudaStream_t st, cs;
     double* host[2] = {nullptr, nullptr};
-    cudaEvent_t done[2] = {nullptr, nullptr};
+    cudaEvent_t cdone[2] = {nullptr, nullptr}, kdone[2] = {nullptr, nullptr};
     ~Staging() {
+      cudaStreamSynchronize(cs);
       cudaStreamSynchronize(st);
       for (int k = 0; k < 2; ++k) {
         if (host[k]) cudaFreeHost(host[k]);
-        if (done[k]) cudaEventDestroy(done[k]);
+        if (cdone[k]) cudaEventDestroy(cdone[k]);
+        if (kdone[k]) cudaEventDestroy(kdone[k]);
       }
     }
-  } stg{b->stream};
+  } stg{b->stream, b->copy_stream};
   double** host = stg.host;
-  cudaEvent_t* done = stg.done;
+  cudaEvent_t* cdone = stg.cdone;
+  cudaEvent_t* kdone = stg.kdone;
   for (int q = 0; q < 2; ++q) {
     if (!direct) CK(cudaMallocHost(&host[q], chunk_doubles * sizeof(double)));
-    CK(cudaEventCreateWithFlags(&done[q], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&cdone[q], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&kdone[q], cudaEventDisableTiming));
   }
+  const cudaStream_t cs = b->copy_stream;
   const Lay L = lay_of(b);
   int rc = 0;
   int q = 0;
   for (int kr0 = 0; kr0 < S2r && !rc; kr0 += kchunk, q ^= 1) {
     const int nk = std::min(kchunk, S2r - kr0);
-    CK(cudaEventSynchronize(done[q]));  // staging buffer q free again
     double* dscr = b->d_scratch + q * chunk_doubles;
     const double* hb = nullptr;
+    CK(cudaStreamWaitEvent(cs, kdone[q], 0));  // scratch q free again
     if (direct) {
       CK(cudaMemcpyAsync(dscr, src_fields + plane * kr0 * 8, plane * nk * 8 * sizeof(double),
-                         cudaMemcpyHostToDevice, b->stream));
+                         cudaMemcpyHostToDevice, cs));
       if (with_bd) {
         CK(cudaMemcpyAsync(dscr + plane * nk * 8, src_bd + plane * kr0 * 3,
-                           plane * nk * 3 * sizeof(double), cudaMemcpyHostToDevice, b->stream));
+                           plane * nk * 3 * sizeof(double), cudaMemcpyHostToDevice, cs));
         hb = src_bd;
       }
     } else {
+      CK(cudaEventSynchronize(cdone[q]));  // host staging q free again
       double* hf = host[q];
       double* hbw = with_bd ? host[q] + plane * nk * 8 : nullptr;
       fill(kr0, nk, hf, hbw);
       hb = hbw;
       CK(cudaMemcpyAsync(dscr, hf, plane * nk * nper * sizeof(double), cudaMemcpyHostToDevice,
-                         b->stream));
+                         cs));
     }
+    CK(cudaEventRecord(cdone[q], cs));
+    CK(cudaStreamWaitEvent(b->stream, cdone[q], 0));
     for (int k = 0; k < 2; ++k)
       aos_to_soa_kernel<<<grid_for(plane * nk), 256, 0, b->stream>>>(
           dscr, 8, planes(b->buf[k], b->ncell), L, gr, S0r, S1r, kr0, nk,
           (k == 0 && hb) ? dscr + plane * nk * 8 : nullptr, b->bd,
           b->bd ? b->bd + b->ncell : nullptr, b->bd ? b->bd + 2 * b->ncell : nullptr);
     cudaError_t e = cudaGetLastError();
-    if (e == cudaSuccess) e = cudaEventRecord(done[q], b->stream);
+    if (e == cudaSuccess) e = cudaEventRecord(kdone[q], b->stream);
     if (e != cudaSuccess) rc = cuda_fail(e, "streamed upload");
   }
   if (rc) return rc;
@@ -1408,16 +1426,37 @@ static int download_impl(ppmlr_gpu_block* b, double* fields, bool interior_only)
     const int kchunk = (int)std::max<size_t>(1, std::min<size_t>(b->n[2], (64ull << 20) / (plane * 64)));
     const size_t half = plane * kchunk * 8;
     if (int rc = ensure_scratch(b, 2 * half * sizeof(double))) return rc;
+    if (int rc = ensure_copy_stream(b)) return rc;
+    // conversion kernels on the block stream, D2H copies on the copy stream
+    // (the copy of chunk q overlaps the kernel of chunk q+1)
+    struct Ev {
+      cudaEvent_t e[4] = {nullptr, nullptr, nullptr, nullptr};
+      ~Ev() {
+        for (auto x : e)
+          if (x) cudaEventDestroy(x);
+      }
+    } ev;
+    for (auto& x : ev.e) CK(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+    cudaEvent_t* kdone = ev.e;      // kernel wrote scratch q
+    cudaEvent_t* cdone = ev.e + 2;  // copy read scratch q
+    const cudaStream_t cs = b->copy_stream;
+    CK(cudaEventRecord(cdone[0], cs));
+    CK(cudaEventRecord(cdone[1], cs));
     int q = 0;
     for (int k0 = 0; k0 < b->n[2]; k0 += kchunk, q ^= 1) {
       const int nk = std::min(kchunk, b->n[2] - k0);
       double* dscr = b->d_scratch + q * half;
+      CK(cudaStreamWaitEvent(b->stream, cdone[q], 0));
       soa_to_interior_kernel<<<grid_for(plane * nk), 256, 0, b->stream>>>(
           dscr, planes(cur_buf(b), b->ncell), L, k0, nk);
       CK(cudaGetLastError());
+      CK(cudaEventRecord(kdone[q], b->stream));
+      CK(cudaStreamWaitEvent(cs, kdone[q], 0));
       CK(cudaMemcpyAsync(fields + plane * k0 * 8, dscr, plane * nk * 64, cudaMemcpyDeviceToHost,
-                         b->stream));
+                         cs));
+      CK(cudaEventRecord(cdone[q], cs));
     }
+    CK(cudaStreamSynchronize(cs));
     CK(cudaStreamSynchronize(b->stream));
     return 0;
   }

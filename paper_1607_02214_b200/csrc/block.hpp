@@ -91,6 +91,8 @@ struct ppmlr_gpu_block {
   double* h_pinned = nullptr;            // 8 doubles pinned scratch
   long step_base = 0;                    // absolute step of d_step == 0
   double* d_scratch = nullptr;           // staging for upload/download
+  cudaStream_t copy_stream = nullptr;    // host<->device chunk copies, overlapped with the
+                                         // layout-conversion kernels on `stream`
   size_t scratch_bytes = 0;
   ppmlr_b200::StepGraph graphs[2][2];    // [parity][cur]
   ppmlr_b200::SweepTiming timing;
