@@ -400,10 +400,21 @@ __device__ __forceinline__ void tma_load_fields(const SweepArgs& A, const SweepM
 }
 
 // Tile t of a (part) launch: the split coordinate runs over its part only.
+#ifndef PPMLR_SWEEP_Z_GROUPS_FIRST
+// z sweeps: claim tiles pencil group (x) first, then y, then the z segment,
+// so the CTAs in flight share the same 72 z-planes (page / DRAM-row
+// locality) instead of spanning the whole z extent
+#define PPMLR_SWEEP_Z_GROUPS_FIRST 1
+#endif
 template <int AXIS>
 __device__ __forceinline__ TileId tile_of_v2(const SweepArgs& A, int t) {
   const int ns = AXIS == 0 ? split_count(A.part, A.cl, A.cr, A.nseg) : A.nseg;
   const int ng = AXIS == 0 ? A.ngroups : split_count(A.part, A.cl, A.cr, A.ngroups);
+  if (AXIS == 2 && PPMLR_SWEEP_Z_GROUPS_FIRST) {
+    const int rest = t / ng;
+    const int v = t - rest * ng, w = rest % A.no;
+    return {rest / A.no, split_unit(A.part, A.cl, A.cr, v), w};
+  }
   const int rest = t / ns;
   const int u = t - rest * ns, v = rest % ng;
   return {AXIS == 0 ? split_unit(A.part, A.cl, A.cr, u) : u,
