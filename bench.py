@@ -408,14 +408,17 @@ def bench_e2e(h, cfg, args, cells):
     final interior into pinned host memory."""
     import torch
     import paper_1607_02214_b200 as P
-    st = P.host_block_state(cfg.specs, (1, 1, 1), cfg.options, 0, cfg.ic)
-    host_in = torch.empty(st["fields"].shape, dtype=torch.float64, pin_memory=True).numpy()
-    host_in[...] = st["fields"]
-    host_bd = None
-    if st["bd"] is not None:  # the dipole travels with the state, also pinned
-        host_bd = torch.empty(st["bd"].shape, dtype=torch.float64, pin_memory=True).numpy()
-        host_bd[...] = st["bd"]
+    # the initial state (and the dipole, which travels with it) evaluated
+    # straight into pinned host buffers: no second host copy (C5 is 39 GB)
+    g = cfg.options.ghost
     nx, ny, nz = (int(s.cells) for s in cfg.specs)
+    shape = (nz + 2 * g, ny + 2 * g, nx + 2 * g)
+    host_in = torch.empty(shape + (8,), dtype=torch.float64, pin_memory=True).numpy()
+    host_bd = None
+    if cfg.options.with_dipole:
+        host_bd = torch.empty(shape + (3,), dtype=torch.float64, pin_memory=True).numpy()
+    st = P.host_block_state(cfg.specs, (1, 1, 1), cfg.options, 0, cfg.ic, fields_out=host_in,
+                            bd_out=host_bd)
     host_out = torch.empty((nz, ny, nx, 8), dtype=torch.float64, pin_memory=True).numpy()
     blk = h.block(0)
     k = args.steps

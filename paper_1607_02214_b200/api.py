@@ -9,6 +9,7 @@ Names, argument meaning and error behaviour follow the reference
 from __future__ import annotations
 
 import ctypes as C
+import math
 import os
 from dataclasses import dataclass, field
 
@@ -428,9 +429,17 @@ def host_block_state(specs, partition=(1, 1, 1), options: HarnessOptions | None 
         kind = int(ic[0])
         p = np.zeros(8)
         p[:len(ic[1])] = ic[1]
-    fidx = np.zeros(cells if kind < 0 else 1, np.int64)  # frozen cells: magnetosphere only
-    fst = np.zeros((cells, 8)) if kind < 0 else np.zeros((1, 8))
-    nf = C.c_int64()
+    # frozen cells (magnetosphere only): the core r < 3 fits a box of
+    # 6 / d_uniform (+ margin) cells per axis
+    cap = 1
+    if kind < 0:
+        cap = 1
+        for a in range(3):
+            cap *= min(spans[a], int(math.ceil(6.0 / float(specs[a].d_uniform))) + 6)
+        cap = max(1, min(cells, cap))
+    fidx = np.zeros(cap, np.int64)
+    fst = np.zeros((cap, 8))
+    nf = C.c_int64(cap if kind < 0 else 0)
     cat_c, cat_s = np.zeros(sum(spans)), np.zeros(sum(spans))
     check(N.lib.ppmlr_host_block_state(_specs3(specs), *partition, C.byref(options.c()), rank,
                                        kind, ptr(p), ptr(fields), ptr(bd),

@@ -898,6 +898,9 @@ int ppmlr_host_block_state(const ppmlr_axis_spec specs[3], int px, int py, int p
       block_fill(hb, ci, f, opts->with_dipole ? &bdv : nullptr);
       if (bd && !bdv.empty()) std::copy(bdv.begin(), bdv.end(), bd);
     }
+    // *n_frozen > 0 on entry: the capacity of frozen_idx / frozen_states
+    if (n_frozen && *n_frozen > 0 && (int64_t)fidx.size() > *n_frozen)
+      invalid("host_block_state: frozen-core capacity too small");
     if (frozen_idx) std::copy(fidx.begin(), fidx.end(), frozen_idx);
     if (frozen_states) std::copy(fst.begin(), fst.end(), frozen_states);
     if (n_frozen) *n_frozen = (int64_t)fidx.size();
