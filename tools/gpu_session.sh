@@ -23,7 +23,8 @@ if [ "${BENCH:-0}" = 1 ]; then
   done
 fi
 if [ "${LAUNCHES:-0}" = 1 ]; then
-  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c ${NLAUNCH:-200} --csv \
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c ${NLAUNCH:-200} \
+    ${LKERNEL:+-k regex:$LKERNEL} --csv \
     --log-file $OUT/launches.csv python bench.py --config ${LCFG:-blast512} --steps 2 --warmup 3 \
     --no-e2e --no-cpu-baseline --no-secondary > $OUT/launches.log 2>&1
   python tools/launch_shares.py $OUT/launches.csv > $OUT/launch_shares.txt 2>&1; cat $OUT/launch_shares.txt | head -12
