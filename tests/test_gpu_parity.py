@@ -414,3 +414,36 @@ def test_distributed_driver_single_rank_nccl(gpu):
     h = _harness(gpu, cfg.specs, cfg.options, cfg.ic)
     h.run(5)
     assert bits_equal(got, h.gather_interior())
+
+
+@pytest.mark.parametrize("n", [16, 64])
+def test_fast_mode_raises_the_reference_failure(gpu, oracle, n):
+    """The fast build detects the same unphysical step as the reference:
+    same exception type at the same step (cfl 2.5 makes Lagrangian interfaces
+    cross), on the runtime tile (16) and the persistent compile-time-tile
+    kernel (64).  (The failing zone may differ within the tolerance of the
+    fast arithmetic, so only the type and the step are compared.)"""
+    from paper_1607_02214_b200.api import AxisSpec, HarnessOptions
+    cube = [AxisSpec.uniform(-0.5, 0.5, n)] * 3
+    ic = (gpu.IC_BLAST, (10.0, 0.1, 0.3))
+    ob = _oracle_from_host(oracle, gpu, cube, HarnessOptions(cfl=2.5), ic)
+    o, k = oracle.opts(cfl=2.5), oracle.consts()
+    err_o = None
+    for s in range(20):
+        try:
+            ob.advance(o, k, s)
+        except oracle.OracleError as e:
+            err_o = (s, e.kind)
+            break
+    h = _harness(gpu, cube, HarnessOptions(cfl=2.5, precision="fast"), ic)
+    err_g = None
+    for s in range(20):
+        try:
+            h.advance()
+        except gpu.Error as e:
+            err_g = (s, type(e).__name__)
+            break
+    assert err_o is not None
+    assert err_g is not None and err_g[0] == err_o[0]
+    assert err_g[1] == {"StepRejected": "StepRejected", "UnphysicalState": "UnphysicalState"}[
+        err_o[1]]
