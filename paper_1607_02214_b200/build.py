@@ -67,6 +67,8 @@ def build_native(force=False, verbose_ptxas=False, defines=(), out=OUT, objdir=O
                    "-o", o, *extra, *[f"-D{d}" for d in defines]]
             if verbose_ptxas:
                 cmd += ["-Xptxas", "-v"]
+            # tuning experiments (tools/variants.py): extra nvcc flags
+            cmd += os.environ.get("PPMLR_NVCC_EXTRA", "").split()
             _run(cmd)
     for src in HOST_UNITS:
         o = os.path.join(objdir, src.replace(".cpp", ".o"))
