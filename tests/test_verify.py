@@ -72,3 +72,12 @@ def test_cli_verify_and_run(gpu, tmp_path, capsys):
                  "--out", str(tmp_path)]) == 0
     assert (tmp_path / "snapshot_000002.bin").exists()
     assert main(["verify", "nosuch"]) == 1
+    # report (ppmlr_main.cpp:107-139): the reference's CSV header and one
+    # row per reference partition shape
+    assert main(["report", "--steps", "1"]) == 0
+    lines = [ln for ln in capsys.readouterr().out.splitlines() if ln]
+    assert lines[0] == ("nx,ny,nz,ranks,tde_units,bytes_per_step,mean_compute_s,"
+                        "mean_transfer_s,predicted_speedup")
+    assert [ln.split(",")[:3] for ln in lines[1:]] == [
+        ["3", "1", "1"], ["3", "3", "3"], ["4", "3", "3"], ["6", "3", "3"], ["4", "5", "5"],
+        ["6", "5", "5"]]
