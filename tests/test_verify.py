@@ -74,6 +74,7 @@ def test_cli_verify_and_run(gpu, tmp_path, capsys):
     assert main(["verify", "nosuch"]) == 1
     # report (ppmlr_main.cpp:107-139): the reference's CSV header and one
     # row per reference partition shape
+    capsys.readouterr()
     assert main(["report", "--steps", "1"]) == 0
     lines = [ln for ln in capsys.readouterr().out.splitlines() if ln]
     assert lines[0] == ("nx,ny,nz,ranks,tde_units,bytes_per_step,mean_compute_s,"
