@@ -240,10 +240,9 @@ class Block:
             pl = list(bp) + [None] * 5
         out = []
         for f in range(3 if dipole else 8):
-            shape = (dims[2], dims[1], st[1])
+            shape = (dims[2], dims[1], dims[0])
             t = torch.as_tensor(_CudaArray(pl[f], shape, (st[2] * 8, st[1] * 8, 8)),
                                 device=f"cuda:{self.device}")
-            t = t[:, :, :dims[0]]
             out.append(t[g:-g, g:-g, g:-g] if interior else t)
         return out
 

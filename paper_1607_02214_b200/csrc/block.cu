@@ -52,13 +52,13 @@ Lay lay_of(const ppmlr_gpu_block* b) {
   l.S1 = b->S[1];
   l.sy = b->sy;
   l.sz = b->sz;
-  l.ncell = b->ncell;
+  l.fs = b->fs;
   return l;
 }
 
-Planes planes(double* base, long long ncell) {
+Planes planes(double* base, long long fs) {
   Planes p;
-  for (int f = 0; f < 8; ++f) p.f[f] = base + f * ncell;
+  for (int f = 0; f < 8; ++f) p.f[f] = base + f * fs;
   return p;
 }
 
@@ -366,6 +366,41 @@ CtxPtrs ctx_of(ppmlr_gpu_block* b) {
 
 double* cur_buf(ppmlr_gpu_block* b) { return b->buf[b->cur]; }
 
+// State layout in HBM.  Both ping-pong buffers and B_d live in one arena,
+// each field a [z][y][x] array with an x pitch P0 (default), or with
+// PPMLR_LAYOUT=rows row-interleaved: for every (y, z) row the 8 fields of
+// buffer 0, the 8 of buffer 1 and the 3 B_d components follow each other
+// ([z][y][field][x], field stride P0, y stride NF*P0), so that a z-sweep
+// tile touches 72 2 MB pages instead of 72 per field.  Measured (DESIGN.md
+// §6): the C5 z sweep -2.4%, the blast 512^3 z sweep +18%; planar stays.
+void set_state_layout(ppmlr_gpu_block* b) {
+  b->P0 = ((b->S[0] + 7) / 8) * 8;
+  const char* env = std::getenv("PPMLR_LAYOUT");
+  const bool rows = env && std::strcmp(env, "rows") == 0;
+  const long long nf = 16 + (b->with_dipole ? 3 : 0);
+  if (!rows) {
+    b->sy = b->P0;
+    b->sz = (long long)b->P0 * b->S[1];
+    b->fs = b->sz * b->S[2];
+    b->ncell = nf * b->fs;
+  } else {
+    b->fs = b->P0;
+    b->sy = nf * b->P0;
+    b->sz = b->sy * b->S[1];
+    b->ncell = b->sz * b->S[2];
+  }
+}
+
+// buf[cur ^ 1] := buf[cur] (all 8 fields, ghosts included)
+cudaError_t copy_state(ppmlr_gpu_block* b, double* dst, const double* src) {
+  if (b->fs == b->P0)
+    return cudaMemcpy2DAsync(dst, sizeof(double) * b->sy, src, sizeof(double) * b->sy,
+                             sizeof(double) * 8 * b->P0, (size_t)b->S[1] * b->S[2],
+                             cudaMemcpyDeviceToDevice, b->stream);
+  return cudaMemcpyAsync(dst, src, sizeof(double) * 8 * b->fs, cudaMemcpyDeviceToDevice,
+                         b->stream);
+}
+
 // Reference message for a decoded error key (sweep / sources / CFL).
 int decode_error(ppmlr_gpu_block* b, unsigned long long key, std::string& msg) {
   const int phase = err_phase(key);
@@ -504,10 +539,10 @@ int launch_sweep(ppmlr_gpu_block* b, int axis, int phase, int part) {
   double* in = b->buf[src];
   double* out = b->buf[src ^ 1];
   for (int f = 0; f < 8; ++f) {
-    A.src[f] = in + f * b->ncell;
-    A.dst[f] = out + f * b->ncell;
+    A.src[f] = in + f * b->fs;
+    A.dst[f] = out + f * b->fs;
   }
-  for (int k = 0; k < 3; ++k) A.bd[k] = b->bd ? b->bd + k * b->ncell : nullptr;
+  for (int k = 0; k < 3; ++k) A.bd[k] = b->bd ? b->bd + k * b->fs : nullptr;
   A.dx = b->ax[axis].dx;
   A.rdx = b->ax[axis].rdx;
   A.slope = b->ax[axis].slope;
@@ -565,7 +600,7 @@ int launch_sweep(ppmlr_gpu_block* b, int axis, int phase, int part) {
 
 int launch_bc(ppmlr_gpu_block* b, int axis_mask, int layers) {
   const Lay L = lay_of(b);
-  Planes s = planes(cur_buf(b), b->ncell);
+  Planes s = planes(cur_buf(b), b->fs);
   BcAxes ax{};
   int na = 0;
   long long work = 0;
@@ -587,11 +622,11 @@ int launch_bc(ppmlr_gpu_block* b, int axis_mask, int layers) {
 
 int launch_cfl(ppmlr_gpu_block* b, unsigned long long step_add) {
   const Lay L = lay_of(b);
-  Planes s = planes(cur_buf(b), b->ncell);
+  Planes s = planes(cur_buf(b), b->fs);
   const long long work = (long long)b->n[0] * b->n[1] * b->n[2];
   const double* bd0 = b->bd ? b->bd : nullptr;
-  const double* bd1 = b->bd ? b->bd + b->ncell : nullptr;
-  const double* bd2 = b->bd ? b->bd + 2 * b->ncell : nullptr;
+  const double* bd1 = b->bd ? b->bd + b->fs : nullptr;
+  const double* bd2 = b->bd ? b->bd + 2 * b->fs : nullptr;
   if (b->with_dipole)
     cfl_kernel<true><<<grid_for(work), 256, 0, b->stream>>>(s, L, bd0, bd1, bd2, b->ax[0].dx,
                                                              b->ax[1].dx, b->ax[2].dx, b->c,
@@ -608,12 +643,12 @@ int launch_cfl(ppmlr_gpu_block* b, unsigned long long step_add) {
 int launch_sources(ppmlr_gpu_block* b, int fuse_cfl, int part) {
   SrcArgs A;
   const int src = part == 2 ? b->cur ^ 1 : b->cur;  // as launch_sweep
-  A.in = planes(b->buf[src], b->ncell);
-  A.out = planes(b->buf[src ^ 1], b->ncell);
+  A.in = planes(b->buf[src], b->fs);
+  A.out = planes(b->buf[src ^ 1], b->fs);
   A.L = lay_of(b);
   A.bd0 = b->bd ? b->bd : nullptr;
-  A.bd1 = b->bd ? b->bd + b->ncell : nullptr;
-  A.bd2 = b->bd ? b->bd + 2 * b->ncell : nullptr;
+  A.bd1 = b->bd ? b->bd + b->fs : nullptr;
+  A.bd2 = b->bd ? b->bd + 2 * b->fs : nullptr;
   A.hm0 = b->ax[0].hm;
   A.hp0 = b->ax[0].hp;
   A.hm1 = b->ax[1].hm;
@@ -662,7 +697,7 @@ int launch_sources(ppmlr_gpu_block* b, int fuse_cfl, int part) {
 int launch_frozen(ppmlr_gpu_block* b) {
   if (b->n_frozen <= 0) return 0;
   frozen_restore_kernel<<<grid_for(b->n_frozen), 256, 0, b->stream>>>(
-      planes(cur_buf(b), b->ncell), b->fidx, b->fstates, b->n_frozen);
+      planes(cur_buf(b), b->fs), b->fidx, b->fstates, b->n_frozen);
   CK(cudaGetLastError());
   b->kernel_launches += 1;
   return 0;
@@ -729,7 +764,7 @@ int build_sweep_maps(ppmlr_gpu_block* b) {
       SweepMaps& m = b->maps[3 * k + a];
       for (int f = 0; f < 11; ++f) {
         if (f >= 8 && !b->bd) break;
-        double* base = f < 8 ? b->buf[k] + f * b->ncell : b->bd + (f - 8) * b->ncell;
+        double* base = f < 8 ? b->buf[k] + f * b->fs : b->bd + (f - 8) * b->fs;
         CUtensorMap* t = f < 8 ? &m.f[f] : &m.bd[f - 8];
         const CUresult r = encode(t, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides,
                                   box[a], elem, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -745,7 +780,7 @@ int build_sweep_maps(ppmlr_gpu_block* b) {
         const cuuint32_t pbox[3] = {(cuuint32_t)PPMLR_KNS::kSrcHX, (cuuint32_t)PPMLR_KNS::kSrcHY, 1};
         for (int f = 0; f < 9; ++f) {
           if (f >= 6 && !b->bd) break;
-          double* base = f < 6 ? b->buf[k] + (1 + f) * b->ncell : b->bd + (f - 6) * b->ncell;
+          double* base = f < 6 ? b->buf[k] + (1 + f) * b->fs : b->bd + (f - 6) * b->fs;
           const CUresult r = encode(&sm.f[f], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims,
                                     strides, pbox, elem, CU_TENSOR_MAP_INTERLEAVE_NONE,
                                     CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -759,7 +794,7 @@ int build_sweep_maps(ppmlr_gpu_block* b) {
       }
       for (int f = 0; f < 8; ++f) {  // results go to the other buffer
         const CUresult r = encode(&m.out[f], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3,
-                                  b->buf[k ^ 1] + f * b->ncell, dims, strides, obox[a], elem,
+                                  b->buf[k ^ 1] + f * b->fs, dims, strides, obox[a], elem,
                                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                                   CU_TENSOR_MAP_L2_PROMOTION_NONE,
                                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -822,10 +857,6 @@ int ppmlr_gpu_block_create(const ppmlr_gpu_block_desc* d, ppmlr_gpu_block** out)
     b->physical[a][0] = d->physical[a][0];
     b->physical[a][1] = d->physical[a][1];
   }
-  b->P0 = ((b->S[0] + 7) / 8) * 8;
-  b->sy = b->P0;
-  b->sz = (long long)b->P0 * b->S[1];
-  b->ncell = b->sz * b->S[2];
   b->c.gamma = d->gamma;
   b->c.mu0 = d->mu0;
   b->c.pressure_floor = d->pressure_floor;
@@ -842,6 +873,7 @@ int ppmlr_gpu_block_create(const ppmlr_gpu_block_desc* d, ppmlr_gpu_block** out)
   b->wind[7] = d->wind_p;
   b->with_dipole = d->with_dipole != 0;
   b->precision = d->precision;
+  set_state_layout(b);
   if (d->boundary == PPMLR_BC_PERIODIC)
     for (int a = 0; a < 3; ++a)
       if (b->physical[a][0] != b->physical[a][1] || (b->physical[a][0] && b->n[a] < d->ghost)) {
@@ -910,17 +942,13 @@ int ppmlr_gpu_block_create(const ppmlr_gpu_block_desc* d, ppmlr_gpu_block** out)
     b->c.r3 = rc5[4];
   }
   cudaError_t e;
-  for (int k = 0; k < 2; ++k) {
-    if ((e = cudaMalloc(&b->buf[k], sizeof(double) * 8 * b->ncell)) != cudaSuccess)
-      return fail(cuda_fail(e, "cudaMalloc(state)"));
-    if ((e = cudaMemset(b->buf[k], 0, sizeof(double) * 8 * b->ncell)) != cudaSuccess)
-      return fail(cuda_fail(e, "cudaMemset(state)"));
-  }
-  if (b->with_dipole) {
-    if ((e = cudaMalloc(&b->bd, sizeof(double) * 3 * b->ncell)) != cudaSuccess)
-      return fail(cuda_fail(e, "cudaMalloc(bd)"));
-    cudaMemset(b->bd, 0, sizeof(double) * 3 * b->ncell);
-  }
+  if ((e = cudaMalloc(&b->arena, sizeof(double) * b->ncell)) != cudaSuccess)
+    return fail(cuda_fail(e, "cudaMalloc(state)"));
+  if ((e = cudaMemset(b->arena, 0, sizeof(double) * b->ncell)) != cudaSuccess)
+    return fail(cuda_fail(e, "cudaMemset(state)"));
+  b->buf[0] = b->arena;
+  b->buf[1] = b->arena + 8 * b->fs;
+  if (b->with_dipole) b->bd = b->arena + 16 * b->fs;
   if ((e = cudaMalloc(&b->d_err, 64)) != cudaSuccess) return fail(cuda_fail(e, "cudaMalloc"));
   b->d_step = b->d_err + 1;
   b->d_min = b->d_err + 2;
@@ -961,8 +989,7 @@ void ppmlr_gpu_block_destroy(ppmlr_gpu_block* b) {
   for (auto& row : b->graphs)
     for (auto& g : row)
       if (g.exec) cudaGraphExecDestroy(g.exec);
-  for (int k = 0; k < 2; ++k) cudaFree(b->buf[k]);
-  cudaFree(b->bd);
+  cudaFree(b->arena);
   for (int a = 0; a < 3; ++a) {
     cudaFree(b->ax[a].dx);
     cudaFree(b->ax[a].slope);
@@ -1160,9 +1187,9 @@ int block_upload_streamed(ppmlr_gpu_block* b, const ChunkFill& fill, bool with_b
     CK(cudaStreamWaitEvent(b->stream, cdone[q], 0));
     for (int k = 0; k < 2; ++k)
       aos_to_soa_kernel<<<grid_for(plane * nk), 256, 0, b->stream>>>(
-          dscr, 8, planes(b->buf[k], b->ncell), L, gr, S0r, S1r, kr0, nk,
+          dscr, 8, planes(b->buf[k], b->fs), L, gr, S0r, S1r, kr0, nk,
           (k == 0 && hb) ? dscr + plane * nk * 8 : nullptr, b->bd,
-          b->bd ? b->bd + b->ncell : nullptr, b->bd ? b->bd + 2 * b->ncell : nullptr);
+          b->bd ? b->bd + b->fs : nullptr, b->bd ? b->bd + 2 * b->fs : nullptr);
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaEventRecord(kdone[q], b->stream);
     if (e != cudaSuccess) rc = cuda_fail(e, "streamed upload");
@@ -1370,8 +1397,8 @@ int block_init_device(ppmlr_gpu_block* b, int kind, const double* params, bool w
   CK(cudaMemsetAsync(d_err, 0, sizeof(int), b->stream));
   const long long total = (long long)b->S[0] * b->S[1] * b->S[2];
   init_state_kernel<<<grid_for(total), 256, 0, b->stream>>>(
-      planes(b->buf[0], b->ncell), planes(b->buf[1], b->ncell), with_bd ? b->bd : nullptr,
-      with_bd ? b->bd + b->ncell : nullptr, with_bd ? b->bd + 2 * b->ncell : nullptr, lay_of(b),
+      planes(b->buf[0], b->fs), planes(b->buf[1], b->fs), with_bd ? b->bd : nullptr,
+      with_bd ? b->bd + b->fs : nullptr, with_bd ? b->bd + 2 * b->fs : nullptr, lay_of(b),
       b->S[0], b->S[1], b->S[2], A, d_err);
   CK(cudaGetLastError());
   int herr = 0;
@@ -1391,8 +1418,8 @@ int block_finish_upload(ppmlr_gpu_block* b) {
   if (b->boundary == PPMLR_BC_MAGNETOSPHERE && b->physical[0][1]) {
     for (int k = 0; k < 2; ++k)
       wind_fill_kernel<<<grid_for((long long)kG * b->n[1] * b->n[2]), 256, 0, b->stream>>>(
-          planes(b->buf[k], b->ncell), L, b->bd, b->bd ? b->bd + b->ncell : nullptr,
-          b->bd ? b->bd + 2 * b->ncell : nullptr, b->wind[0], b->wind[7], b->wind[1],
+          planes(b->buf[k], b->fs), L, b->bd, b->bd ? b->bd + b->fs : nullptr,
+          b->bd ? b->bd + 2 * b->fs : nullptr, b->wind[0], b->wind[7], b->wind[1],
           b->wind[2], b->wind[3], b->wind[4], b->wind[5], b->wind[6]);
     CK(cudaGetLastError());
   }
@@ -1448,7 +1475,7 @@ static int download_impl(ppmlr_gpu_block* b, double* fields, bool interior_only)
       double* dscr = b->d_scratch + q * half;
       CK(cudaStreamWaitEvent(b->stream, cdone[q], 0));
       soa_to_interior_kernel<<<grid_for(plane * nk), 256, 0, b->stream>>>(
-          dscr, planes(cur_buf(b), b->ncell), L, k0, nk);
+          dscr, planes(cur_buf(b), b->fs), L, k0, nk);
       CK(cudaGetLastError());
       CK(cudaEventRecord(kdone[q], b->stream));
       CK(cudaStreamWaitEvent(cs, kdone[q], 0));
@@ -1468,7 +1495,7 @@ static int download_impl(ppmlr_gpu_block* b, double* fields, bool interior_only)
   for (int kr0 = 0; kr0 < S2r; kr0 += kchunk) {
     const int nk = std::min(kchunk, S2r - kr0);
     soa_to_aos_kernel<<<grid_for(plane * nk), 256, 0, b->stream>>>(
-        b->d_scratch, planes(cur_buf(b), b->ncell), L, gr, S0r, S1r, kr0, nk);
+        b->d_scratch, planes(cur_buf(b), b->fs), L, gr, S0r, S1r, kr0, nk);
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(fields + plane * kr0 * 8, b->d_scratch, plane * nk * 64,
                        cudaMemcpyDeviceToHost, b->stream));
@@ -1495,7 +1522,7 @@ int ppmlr_gpu_block_snapshot_capture(ppmlr_gpu_block* b) {
   CK(cudaStreamSynchronize(b->snap_stream));
   if (!b->d_snap) CK(cudaMalloc(&b->d_snap, sizeof(double) * 8 * (size_t)cells));
   interior_planes_kernel<<<grid_for(cells), 256, 0, b->stream>>>(
-      b->d_snap, planes(cur_buf(b), b->ncell), lay_of(b));
+      b->d_snap, planes(cur_buf(b), b->fs), lay_of(b));
   CK(cudaGetLastError());
   b->kernel_launches += 1;
   CK(cudaEventRecord(b->snap_ready, b->stream));
@@ -1599,8 +1626,7 @@ int ppmlr_gpu_block_sweep(ppmlr_gpu_block* b, int axis, double dt) {
   if (int rc = block_set_dt(b, dt)) return rc;
   // The sweep writes only interior cells of the other buffer; carry the
   // untouched cells (ghosts) over so the block behaves in place.
-  CK(cudaMemcpyAsync(b->buf[b->cur ^ 1], b->buf[b->cur], sizeof(double) * 8 * b->ncell,
-                     cudaMemcpyDeviceToDevice, b->stream));
+  CK(copy_state(b, b->buf[b->cur ^ 1], b->buf[b->cur]));
   if (int rc = launch_sweep(b, axis, kPhaseSweep0 + axis)) return rc;
   return 0;
 }
@@ -1609,8 +1635,7 @@ int ppmlr_gpu_block_sources(ppmlr_gpu_block* b, double dt) {
   b->dt_valid = false;  // state or dt slot changes
   CK(cudaSetDevice(b->device));
   if (int rc = block_set_dt(b, dt)) return rc;
-  CK(cudaMemcpyAsync(b->buf[b->cur ^ 1], b->buf[b->cur], sizeof(double) * 8 * b->ncell,
-                     cudaMemcpyDeviceToDevice, b->stream));
+  CK(copy_state(b, b->buf[b->cur ^ 1], b->buf[b->cur]));
   // standalone apply_sources: no frozen override, no fused CFL
   const long long nf = b->n_frozen;
   b->n_frozen = 0;
@@ -1753,7 +1778,7 @@ int ppmlr_gpu_block_pack_face(ppmlr_gpu_block* b, int face, int layers, double* 
   }
   const int axis = face / 2;
   const long long work = (long long)layers * b->n[(axis + 1) % 3] * b->n[(axis + 2) % 3];
-  pack_kernel<<<grid_for(work), 256, 0, b->stream>>>(planes(cur_buf(b), b->ncell), lay_of(b),
+  pack_kernel<<<grid_for(work), 256, 0, b->stream>>>(planes(cur_buf(b), b->fs), lay_of(b),
                                                        face, layers, dev_buf);
   CK(cudaGetLastError());
   return 0;
@@ -1769,7 +1794,7 @@ int ppmlr_gpu_block_unpack_face(ppmlr_gpu_block* b, int face, int layers,
   }
   const int axis = face / 2;
   const long long work = (long long)layers * b->n[(axis + 1) % 3] * b->n[(axis + 2) % 3];
-  unpack_kernel<<<grid_for(work), 256, 0, b->stream>>>(planes(cur_buf(b), b->ncell),
+  unpack_kernel<<<grid_for(work), 256, 0, b->stream>>>(planes(cur_buf(b), b->fs),
                                                          lay_of(b), face, layers, dev_buf);
   CK(cudaGetLastError());
   return 0;
@@ -1787,7 +1812,7 @@ int ppmlr_gpu_block_copy_face(ppmlr_gpu_block* dst, int face, ppmlr_gpu_block* s
   }
   const long long work = (long long)layers * dst->n[(axis + 1) % 3] * dst->n[(axis + 2) % 3];
   copy_face_kernel<<<grid_for(work), 256, 0, dst->stream>>>(
-      planes(cur_buf(dst), dst->ncell), lay_of(dst), planes(cur_buf(src), src->ncell),
+      planes(cur_buf(dst), dst->fs), lay_of(dst), planes(cur_buf(src), src->fs),
       lay_of(src), face, layers);
   CK(cudaGetLastError());
   return 0;
@@ -1868,7 +1893,7 @@ int ppmlr_gpu_block_synchronize(ppmlr_gpu_block* b) {
 
 int ppmlr_gpu_block_state_view(ppmlr_gpu_block* b, double** field_planes, long long* strides,
                                int* dims) {
-  for (int f = 0; f < 8; ++f) field_planes[f] = cur_buf(b) + (long long)f * b->ncell;
+  for (int f = 0; f < 8; ++f) field_planes[f] = cur_buf(b) + (long long)f * b->fs;
   strides[0] = 1;
   strides[1] = b->sy;
   strides[2] = b->sz;
@@ -1888,7 +1913,7 @@ int ppmlr_gpu_block_init_ic(ppmlr_gpu_block* b, int kind, const double* params) 
 }
 
 int ppmlr_gpu_block_dipole_view(ppmlr_gpu_block* b, double** bd_planes) {
-  for (int a = 0; a < 3; ++a) bd_planes[a] = b->bd ? b->bd + (long long)a * b->ncell : nullptr;
+  for (int a = 0; a < 3; ++a) bd_planes[a] = b->bd ? b->bd + (long long)a * b->fs : nullptr;
   return b->bd ? 1 : 0;
 }
 

@@ -59,8 +59,10 @@ struct ppmlr_gpu_block {
   int S[3] = {0, 0, 0};      // n + 8
   int P0 = 0;                // padded x pitch (>= S[0], multiple of 8)
   long long sx = 1, sy = 0, sz = 0;
-  long long ncell = 0;       // elements per field plane
-  double* buf[2] = {nullptr, nullptr};  // 8 planes each
+  long long ncell = 0;       // elements of the arena (both buffers + B_d)
+  long long fs = 0;          // field stride: planar S[2]*sz, row-interleaved P0
+  double* arena = nullptr;   // one allocation: buf[0], buf[1], bd
+  double* buf[2] = {nullptr, nullptr};  // 8 fields each
   int cur = 0;               // buffer holding the current state
   double* bd = nullptr;      // 3 planes or nullptr
   ppmlr_b200::DevAxis ax[3];

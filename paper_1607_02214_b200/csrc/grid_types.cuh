@@ -12,7 +12,7 @@ constexpr unsigned long long kInfBits = 0x7FF0000000000000ull;
 struct Lay {
   int n0, n1, n2;
   int P0, S1;
-  long long sy, sz, ncell;
+  long long sy, sz, fs;  // y / z cell strides; fs: distance between two fields
   __host__ __device__ long long idx(int i, int j, int k) const {  // interior coords
     return (long long)(i + kG) + sy * (j + kG) + sz * (k + kG);
   }

@@ -163,3 +163,25 @@ def test_fast_partial_compile_time_tiles_within_tolerance(gpu, dims, dipole):
         h.close()
     l1, linf = rel_errors(out["fast"], out["strict"])
     assert np.all(l1 <= FAST_L1) and np.all(linf <= FAST_LINF), (l1, linf)
+
+
+@pytest.mark.parametrize("name", ["blast_64_10", "dipole_64_6"])
+@pytest.mark.parametrize("precision", ["strict", "fast"])
+def test_row_interleaved_layout_reproduces_reference(gpu, monkeypatch, name, precision):
+    """PPMLR_LAYOUT=rows (block.cu set_state_layout: the fields of both
+    buffers and B_d interleaved per x row) changes only addresses: the
+    strict build still reproduces the reference digest, the fast build the
+    planar fast result bit for bit."""
+    rec = GOLD[name]
+    out = {}
+    for lay in ("planar", "rows"):
+        monkeypatch.setenv("PPMLR_LAYOUT", lay)
+        h = _harness(gpu, rec, precision)
+        h.run(rec["steps"])
+        out[lay] = h.gather_interior()
+        views = h.block(0).state_view()
+        assert np.array_equal(np.stack([v.cpu().numpy() for v in views], axis=-1), out[lay])
+        h.close()
+    if precision == "strict":
+        assert digest(out["rows"]) == rec["final_sha"]
+    assert np.array_equal(out["rows"].view(np.int64), out["planar"].view(np.int64))
