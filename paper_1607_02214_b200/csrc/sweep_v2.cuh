@@ -45,11 +45,12 @@ namespace PPMLR_KNS {
 #endif
 #endif
 
-template <int AXIS, bool DIPOLE, int NP, int TL, class Ops, class Prefetch>
+template <int AXIS, bool DIPOLE, int NP, int TL, class Ops, class Prefetch, class Sync>
 __device__ __forceinline__ bool sweep_tile_v2(const SweepArgs& A, const SweepMaps& M,
                                               const TileId id, double* smem, double* FLD,
                                               double* RSB, unsigned long long* s_err,
-                                              bool& stored, const Prefetch& prefetch) {
+                                              bool& stored, const Prefetch& prefetch,
+                                              const Sync& lsync, bool& moved) {
   bool tbad = false;
   // TL > 0: the compile-time tile; TL == 0: the block's runtime tile L + 8
   const int TLr = TL > 0 ? TL : A.L + 8;
@@ -115,7 +116,7 @@ __device__ __forceinline__ bool sweep_tile_v2(const SweepArgs& A, const SweepMap
       }
     }
   }
-  __syncthreads();
+  lsync(0);
 
   // ---- P3: traced states of zones [2, zmax]; L -> LFT, R in registers ------
   double R[8];
@@ -179,7 +180,7 @@ __device__ __forceinline__ bool sweep_tile_v2(const SweepArgs& A, const SweepMap
       all8(FlatTag<false>{});
     tbad |= o.bad;
   }
-  __syncthreads();
+  lsync(1);
 
   // ---- P4: edge m = s + 1 in [3, zmax] by the thread of zone s ------------
   bool mv = false;
@@ -213,6 +214,7 @@ __device__ __forceinline__ bool sweep_tile_v2(const SweepArgs& A, const SweepMap
     for (int v = 0; v < 8; ++v) TR[v * T + ci + SS] = f[v];
   }
   const bool moving = __syncthreads_or(mv);
+  moved = moving;
   if (PPMLR_SWEEP_V2_RSMEM) prefetch();  // the right states in RSB are consumed
 
   // ---- P7: Lagrangian update of zones [3, zmax-1] -> LFT -------------------
@@ -265,7 +267,7 @@ __device__ __forceinline__ bool sweep_tile_v2(const SweepArgs& A, const SweepMap
       for (int v = 0; v < 8; ++v) FLD[v * T + ci] = cons[v];
     }
   }
-  __syncthreads();
+  lsync(2);
 
   const bool e8 = live && s >= 4 && s <= TLv - 4;
   if (moving) {
@@ -278,7 +280,7 @@ __device__ __forceinline__ bool sweep_tile_v2(const SweepArgs& A, const SweepMap
         TR[v * T + ci] = slope_with(cv[-SS], cv[0], cv[SS], sc);
       }
     }
-    __syncthreads();
+    lsync(3);
     // ---- P8: slivers at edges [4, TLv-4] --------------------------------
     double sl[8];
 #pragma unroll
@@ -315,12 +317,12 @@ __device__ __forceinline__ bool sweep_tile_v2(const SweepArgs& A, const SweepMap
         tbad |= o.bad;
       }
     }
-    __syncthreads();
+    lsync(4);
     if (e8) {
 #pragma unroll
       for (int v = 0; v < 8; ++v) TR[v * T + ci] = sl[v];
     }
-    __syncthreads();
+    lsync(5);
   }
 
   // ---- P9: remap, cons_to_prim, store (zones [4, TLv-5]) ------------------
@@ -435,6 +437,17 @@ __device__ __forceinline__ TileId tile_of_v2(const SweepArgs& A, int t) {
           AXIS == 0 ? v : split_unit(A.part, A.cl, A.cr, v), rest / ng};
 }
 
+// Sites (bit j of the mask) whose phase barrier is a neighbour-warp one.
+// Measured (fast): P0|P3 + P3|P4 local: C5 sweep -2.7%, blast neutral, C2
+// -0.4%; the Lagrangian / remap sites local too: blast +1.5-1.8%.  Strict
+// build (right states in registers): C5 +3.5%, blast +2% -- off.
+#ifndef PPMLR_SWEEP_V2_LSYNC
+#ifdef PPMLR_FAST_MATH
+#define PPMLR_SWEEP_V2_LSYNC 3
+#else
+#define PPMLR_SWEEP_V2_LSYNC 0
+#endif
+#endif
 #ifndef PPMLR_SWEEP_V2_MINB
 #define PPMLR_SWEEP_V2_MINB 3
 #endif
@@ -453,6 +466,14 @@ __global__ void __launch_bounds__(NP*(TL > 0 ? TL : kSweepTL), PPMLR_SWEEP_V2_MI
   extern __shared__ __align__(128) double smem[];
   __shared__ unsigned long long s_err;
   __shared__ __align__(8) unsigned long long s_mbar[2];
+  // neighbour-warp phase barriers (PPMLR_SWEEP_V2_LSYNC): one mbarrier per
+  // warp and sync site (sites 0-2 every tile, 3-5 moving tiles only), plus
+  // the "previous result box read" signal that gates the RSB writes of P3
+  constexpr int kNW = TL > 0 ? NP * TL / 32 : 1;
+  constexpr bool kLocal = PPMLR_SWEEP_V2_LSYNC && TL > 0 && (NP * TL) % 32 == 0;
+  __shared__ __align__(8) unsigned long long s_lbar[kLocal ? 6 * kNW : 1];
+  __shared__ __align__(8) unsigned long long s_drain;
+  __shared__ unsigned s_nmov;
   // the claimed tile of each buffer, decoded once by the elected thread:
   // {t, seg, grp, oc}
   __shared__ int s_tile[2][4];
@@ -471,6 +492,13 @@ __global__ void __launch_bounds__(NP*(TL > 0 ? TL : kSweepTL), PPMLR_SWEEP_V2_MI
     s_err = kNoError;
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&s_mbar[0])) : "memory");
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&s_mbar[1])) : "memory");
+    if (kLocal) {
+      for (int j = 0; j < 6 * kNW; ++j)
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 32;" ::"r"(smem_u32(&s_lbar[j]))
+                     : "memory");
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&s_drain)) : "memory");
+      s_nmov = 0;
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     const TileId id0 = claim(0, blockIdx.x);
@@ -494,7 +522,28 @@ __global__ void __launch_bounds__(NP*(TL > 0 ? TL : kSweepTL), PPMLR_SWEEP_V2_MI
       // the other buffer held the previous tile's result box: its TMA store
       // must have read it before it is reused (scratch, then the next fields)
       asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      if (kLocal)
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&s_drain))
+                     : "memory");
     }
+    // Phase barrier j of the tile: with kLocal, warp w waits only for warps
+    // w-1 and w+1 (every smem dependency of a phase on the one before spans
+    // at most 2 strip positions = one neighbouring warp; the staged result
+    // box of P9 lands at most 28 threads back, outside what warp w-2 reads)
+    auto lsync = [&](int j) {
+      if (!kLocal || !((PPMLR_SWEEP_V2_LSYNC >> j) & 1)) {
+        __syncthreads();
+        return;
+      }
+      const int w = threadIdx.x >> 5;
+      const unsigned par = j < 3 ? (unsigned)i & 1u : s_nmov & 1u;
+      unsigned long long* b = s_lbar + j * kNW;
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b + w)) : "memory");
+      __syncwarp();
+      if (j == 0 && PPMLR_SWEEP_V2_RSMEM) mbar_wait(&s_drain, (unsigned)i & 1u);
+      if (w > 0) mbar_wait(b + w - 1, par);
+      if (w + 1 < kNW) mbar_wait(b + w + 1, par);
+    };
     auto prefetch = [&]() {
       if (threadIdx.x == 0 && tn < ntiles) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -504,10 +553,13 @@ __global__ void __launch_bounds__(NP*(TL > 0 ? TL : kSweepTL), PPMLR_SWEEP_V2_MI
     if (!PPMLR_SWEEP_V2_RSMEM) prefetch();
     mbar_wait(&s_mbar[buf], (unsigned)(i >> 1) & 1u);
     bool stored = false;
+    bool moved = false;
     const bool bad = sweep_tile_v2<AXIS, DIPOLE, NP, TL, MainOps>(A, M, id, smem, FLD, NXT,
-                                                                  &s_err, stored, prefetch);
+                                                                  &s_err, stored, prefetch, lsync,
+                                                                  moved);
     const bool any_bad = __syncthreads_or(bad);
     if (threadIdx.x == 0) {
+      if (kLocal && moved) ++s_nmov;
       if (stored) {
         const int a0 = id.seg * A.L + 4, g = id.grp * NP + 4, o = id.oc + 4;
         const int c0 = AXIS == 0 ? a0 : g;
