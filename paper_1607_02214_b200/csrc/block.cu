@@ -225,6 +225,26 @@ __global__ void wind_fill_kernel(Planes s, Lay L, const double* bd0, const doubl
   }
 }
 
+// B_d planes -> z-bricks (SweepArgs::bdz): one thread per brick element,
+// the padding pencils of a partial last x group are zero.
+// axis 1: o = z, strip position y; axis 2: o = y, strip position z.
+__global__ void bd_bricks_kernel(double* __restrict__ bdz, const double* __restrict__ bd,
+                                 long long fs, Lay L, int axis, int ngx, int s2, long long cs) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < 3 * cs;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(e / cs);
+    const long long r = e - c * cs;
+    const int p = (int)(r & 3);
+    const long long rq = r >> 2;
+    const int q = (int)(rq % s2);
+    const long long ox = rq / s2;
+    const int xg = (int)(ox % ngx), o = (int)(ox / ngx);
+    const int x = xg * 4 + p;
+    const long long yz = axis == 2 ? L.sy * (o + kG) + L.sz * q : L.sy * q + L.sz * (o + kG);
+    bdz[e] = x < L.n0 ? bd[c * fs + (x + kG) + yz] : 0.0;
+  }
+}
+
 // Standalone compute_dt over the interior; min into ctx.min.
 template <bool DIPOLE>
 __global__ void cfl_kernel(Planes s, Lay L, const double* bd0, const double* bd1,
@@ -543,6 +563,10 @@ int launch_sweep(ppmlr_gpu_block* b, int axis, int phase, int part) {
     A.dst[f] = out + f * b->fs;
   }
   for (int k = 0; k < 3; ++k) A.bd[k] = b->bd ? b->bd + k * b->fs : nullptr;
+  A.bdz = axis > 0 ? b->bdz[axis - 1] : nullptr;
+  A.bdz_cs = axis > 0 ? b->bdz_cs[axis - 1] : 0;
+  A.bdz_ngx = b->bdz_ngx;
+  A.bdz_s2 = b->S[axis];
   A.dx = b->ax[axis].dx;
   A.rdx = b->ax[axis].rdx;
   A.slope = b->ax[axis].slope;
@@ -949,6 +973,16 @@ int ppmlr_gpu_block_create(const ppmlr_gpu_block_desc* d, ppmlr_gpu_block** out)
   b->buf[0] = b->arena;
   b->buf[1] = b->arena + 8 * b->fs;
   if (b->with_dipole) b->bd = b->arena + 16 * b->fs;
+  if (b->with_dipole) {  // y and z bricks: +2 x 3 x 8 B per cell (C5 +29 GB)
+    b->bdz_ngx = (b->n[0] + 3) / 4;
+    for (int a = 1; a < 3; ++a) {
+      b->bdz_cs[a - 1] = (long long)b->n[a == 1 ? 2 : 1] * b->bdz_ngx * b->S[a] * 4;
+      if ((e = cudaMalloc(&b->bdz[a - 1], sizeof(double) * 3 * b->bdz_cs[a - 1])) !=
+          cudaSuccess)
+        return fail(cuda_fail(e, "cudaMalloc(bd bricks)"));
+    }
+    b->bd_dirty = true;
+  }
   if ((e = cudaMalloc(&b->d_err, 64)) != cudaSuccess) return fail(cuda_fail(e, "cudaMalloc"));
   b->d_step = b->d_err + 1;
   b->d_min = b->d_err + 2;
@@ -990,6 +1024,8 @@ void ppmlr_gpu_block_destroy(ppmlr_gpu_block* b) {
     for (auto& g : row)
       if (g.exec) cudaGraphExecDestroy(g.exec);
   cudaFree(b->arena);
+  cudaFree(b->bdz[0]);
+  cudaFree(b->bdz[1]);
   for (int a = 0; a < 3; ++a) {
     cudaFree(b->ax[a].dx);
     cudaFree(b->ax[a].slope);
@@ -1124,6 +1160,7 @@ int block_upload_streamed(ppmlr_gpu_block* b, const ChunkFill& fill, bool with_b
   const int S0r = b->n[0] + 2 * gr, S1r = b->n[1] + 2 * gr, S2r = b->n[2] + 2 * gr;
   const size_t plane = (size_t)S0r * S1r;
   with_bd = with_bd && b->with_dipole && b->bd;
+  if (with_bd) b->bd_dirty = true;
   const int nper = with_bd ? 11 : 8;
   const int kchunk = (int)std::max<size_t>(1, std::min<size_t>(S2r, (64ull << 20) / (plane * 8 * nper)));
   const size_t chunk_doubles = plane * kchunk * nper;
@@ -1364,6 +1401,7 @@ int block_init_device(ppmlr_gpu_block* b, int kind, const double* params, bool w
   CK(cudaSetDevice(b->device));
   CK(cudaStreamSynchronize(b->stream));
   with_bd = with_bd && b->with_dipole && b->bd;
+  if (with_bd) b->bd_dirty = true;
   InitArgs A{};
   A.kind = kind;
   A.mu0 = b->c.mu0;
@@ -1414,6 +1452,15 @@ int block_init_device(ppmlr_gpu_block* b, int kind, const double* params, bool w
 int block_finish_upload(ppmlr_gpu_block* b) {
   b->dt_valid = false;  // state or dt slot changes
   const Lay L = lay_of(b);
+  if (b->bd_dirty) {
+    for (int a = 1; a < 3; ++a)
+      if (b->bdz[a - 1]) {
+        bd_bricks_kernel<<<grid_for(3 * b->bdz_cs[a - 1]), 256, 0, b->stream>>>(
+            b->bdz[a - 1], b->bd, b->fs, L, a, b->bdz_ngx, b->S[a], b->bdz_cs[a - 1]);
+        CK(cudaGetLastError());
+      }
+    b->bd_dirty = false;
+  }
   // Magnetosphere: constant sunward shell in both buffers.
   if (b->boundary == PPMLR_BC_MAGNETOSPHERE && b->physical[0][1]) {
     for (int k = 0; k < 2; ++k)

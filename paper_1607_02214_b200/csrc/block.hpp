@@ -65,6 +65,10 @@ struct ppmlr_gpu_block {
   double* buf[2] = {nullptr, nullptr};  // 8 fields each
   int cur = 0;               // buffer holding the current state
   double* bd = nullptr;      // 3 planes or nullptr
+  double* bdz[2] = {nullptr, nullptr};  // B_d bricks for the y / z sweeps (SweepArgs::bdz)
+  long long bdz_cs[2] = {0, 0};         // elements per brick component
+  int bdz_ngx = 0;           // x groups of 4 interior cells
+  bool bd_dirty = false;     // bd written since the bricks were built
   ppmlr_b200::DevAxis ax[3];
   std::vector<double> h_centers[3], h_spacings[3];  // kG-ghost windows
   int physical[3][2] = {{0, 0}, {0, 0}, {0, 0}};

@@ -154,6 +154,15 @@ struct SweepArgs {
   // a neighbour needs -- and "interior" in [cl, cr).  part 0: every tile,
   // 1: boundary units only, 2: interior units only.
   int part, cl, cr;
+  // y / z sweeps with the dipole: B_d in bricks along the sweep axis
+  // (block.cu bd_bricks_kernel): component c, interior index o of the other
+  // axis, x group xg (4 cells from x = 4), strip position q, pencil p at
+  // bdz[c * bdz_cs + ((o * bdz_ngx + xg) * bdz_s2 + q) * 4 + p] -- a tile's
+  // 72 x 4 values are one contiguous 2.3 KB run instead of 72 rows of 32 B
+  // (z: 72 planes, i.e. 2 MB pages, apart)
+  const double* bdz;
+  long long bdz_cs;
+  int bdz_ngx, bdz_s2;
 };
 
 

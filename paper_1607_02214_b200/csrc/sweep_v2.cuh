@@ -45,6 +45,13 @@ namespace PPMLR_KNS {
 #endif
 #endif
 
+#ifndef PPMLR_SWEEP_BD_BRICKS
+#define PPMLR_SWEEP_BD_BRICKS 1  // z sweeps read B_d from its z-brick copy (SweepArgs::bdz)
+#endif
+#ifndef PPMLR_SWEEP_BD_BRICKS_Y
+#define PPMLR_SWEEP_BD_BRICKS_Y 1  // ... and y sweeps from a y-brick copy
+#endif
+
 template <int AXIS, bool DIPOLE, int NP, int TL, class Ops, class Prefetch, class Sync>
 __device__ __forceinline__ bool sweep_tile_v2(const SweepArgs& A, const SweepMaps& M,
                                               const TileId id, double* smem, double* FLD,
@@ -90,6 +97,8 @@ __device__ __forceinline__ bool sweep_tile_v2(const SweepArgs& A, const SweepMap
     return (unsigned long long)t1 + (unsigned long long)A.nb * (unsigned long long)t2;
   };
   constexpr int a = AXIS, b = (AXIS + 1) % 3, d = (AXIS + 2) % 3;
+  constexpr bool kBricks =
+      (AXIS == 2 && PPMLR_SWEEP_BD_BRICKS) || (AXIS == 1 && PPMLR_SWEEP_BD_BRICKS_Y);
   constexpr int fof[8] = {0, 1 + a, 1 + b, 1 + d, 4 + a, 4 + b, 4 + d, 7};
 
   // ---- P0: cf and primitive slopes ----------------------------------------
@@ -98,7 +107,11 @@ __device__ __forceinline__ bool sweep_tile_v2(const SweepArgs& A, const SweepMap
 #pragma unroll
     for (int f = 0; f < 8; ++f) qv[f] = FLD[f * T + ci];
     Ops o;
-    if (DIPOLE) {  // B_d from global memory (L1/L2: 3 planes, read twice per sweep)
+    if (DIPOLE && kBricks) {  // B_d bricks along the sweep axis (coalesced)
+      const long long zo = ((long long)(oc * A.bdz_ngx + grp) * A.bdz_s2 + q) * 4 + p;
+      CF[ci] = fast_speed3<AXIS, Ops, true>(qv, __ldg(A.bdz + zo), __ldg(A.bdz + A.bdz_cs + zo),
+                                            __ldg(A.bdz + 2 * A.bdz_cs + zo), k, o);
+    } else if (DIPOLE) {  // B_d from global memory (L1/L2: 3 planes, read twice per sweep)
       const long long off = (long long)(g0 + p + 4) * A.stride_g +
                             (long long)(oc + 4) * A.stride_o + (long long)q * A.stride_a;
       CF[ci] = fast_speed3<AXIS, Ops, true>(qv, __ldg(A.bd[0] + off), __ldg(A.bd[1] + off),
@@ -187,7 +200,16 @@ __device__ __forceinline__ bool sweep_tile_v2(const SweepArgs& A, const SweepMap
   if (live && s >= 2 && s <= zmax - 1) {
     double f[8];
     double bl[3] = {0.0, 0.0, 0.0}, br[3] = {0.0, 0.0, 0.0};
-    if (DIPOLE) {  // the two zones' B_d in strip order (a, b, d)
+    if (DIPOLE && kBricks) {  // bricks, components in strip order (a, b, d)
+      const long long zo = ((long long)(oc * A.bdz_ngx + grp) * A.bdz_s2 + q) * 4 + p;
+      constexpr int ja = AXIS, jb = (AXIS + 1) % 3, jd = (AXIS + 2) % 3;
+      bl[0] = __ldg(A.bdz + ja * A.bdz_cs + zo);
+      bl[1] = __ldg(A.bdz + jb * A.bdz_cs + zo);
+      bl[2] = __ldg(A.bdz + jd * A.bdz_cs + zo);
+      br[0] = __ldg(A.bdz + ja * A.bdz_cs + zo + 4);
+      br[1] = __ldg(A.bdz + jb * A.bdz_cs + zo + 4);
+      br[2] = __ldg(A.bdz + jd * A.bdz_cs + zo + 4);
+    } else if (DIPOLE) {  // the two zones' B_d in strip order (a, b, d)
       const long long off = (long long)(g0 + p + 4) * A.stride_g +
                             (long long)(oc + 4) * A.stride_o + (long long)q * A.stride_a;
       constexpr int ja = AXIS, jb = (AXIS + 1) % 3, jd = (AXIS + 2) % 3;
