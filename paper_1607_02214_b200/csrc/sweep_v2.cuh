@@ -45,6 +45,27 @@ namespace PPMLR_KNS {
 #endif
 #endif
 
+// z sweeps: right states in registers and the next tile's fields requested
+// at the tile start.  A z result box (64 rows of 32 B, 64 planes apart)
+// takes long to drain through the TMA store; with the right states in the
+// other buffer every warp waited for it before P3 (the largest stall of
+// the blast z sweep, profiles/r02).  Blast sweep -0.8%, C5 neutral; a
+// request after P4 instead: -0.1%.
+#ifndef PPMLR_SWEEP_V2_RSMEM_Z
+#define PPMLR_SWEEP_V2_RSMEM_Z 0
+#endif
+#ifndef PPMLR_SWEEP_V2_LATE_PF_Z
+#define PPMLR_SWEEP_V2_LATE_PF_Z 0
+#endif
+template <int AXIS>
+__device__ constexpr bool rs_of() {
+  return PPMLR_SWEEP_V2_RSMEM && (AXIS != 2 || PPMLR_SWEEP_V2_RSMEM_Z);
+}
+template <int AXIS>
+__device__ constexpr bool late_pf() {
+  return rs_of<AXIS>() || (AXIS == 2 && PPMLR_SWEEP_V2_LATE_PF_Z);
+}
+
 #ifndef PPMLR_SWEEP_BD_BRICKS
 #define PPMLR_SWEEP_BD_BRICKS 1  // z sweeps read B_d from its z-brick copy (SweepArgs::bdz)
 #endif
@@ -182,7 +203,7 @@ __device__ __forceinline__ bool sweep_tile_v2(const SweepArgs& A, const SweepMap
           if (badR) R[v] = own;
         }
       }
-      if (PPMLR_SWEEP_V2_RSMEM) {
+      if (rs_of<AXIS>()) {
 #pragma unroll
         for (int v = 0; v < 8; ++v) RSB[v * T + ci] = R[v];
       }
@@ -223,7 +244,7 @@ __device__ __forceinline__ bool sweep_tile_v2(const SweepArgs& A, const SweepMap
     const SmemVec qr{LFT + ci + SS, T};
     Ops o;
     double us;
-    if (PPMLR_SWEEP_V2_RSMEM) {
+    if (rs_of<AXIS>()) {
       const SmemVec ql{RSB + ci, T};
       us = solve_edge<SmemVec, SmemVec, Ops, DIPOLE>(ql, qr, bl, br, k, f, o);
     } else {
@@ -237,7 +258,7 @@ __device__ __forceinline__ bool sweep_tile_v2(const SweepArgs& A, const SweepMap
   }
   const bool moving = __syncthreads_or(mv);
   moved = moving;
-  if (PPMLR_SWEEP_V2_RSMEM) prefetch();  // the right states in RSB are consumed
+  if (late_pf<AXIS>()) prefetch();  // the right states in RSB are consumed
 
   // ---- P7: Lagrangian update of zones [3, zmax-1] -> LFT -------------------
   // (moving tiles: every cell's conserved state -> FLD for the remap)
@@ -562,7 +583,7 @@ __global__ void __launch_bounds__(NP*(TL > 0 ? TL : kSweepTL), PPMLR_SWEEP_V2_MI
       unsigned long long* b = s_lbar + j * kNW;
       asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b + w)) : "memory");
       __syncwarp();
-      if (j == 0 && PPMLR_SWEEP_V2_RSMEM) mbar_wait(&s_drain, (unsigned)i & 1u);
+      if (j == 0 && rs_of<AXIS>()) mbar_wait(&s_drain, (unsigned)i & 1u);
       if (w > 0) mbar_wait(b + w - 1, par);
       if (w + 1 < kNW) mbar_wait(b + w + 1, par);
     };
@@ -572,7 +593,7 @@ __global__ void __launch_bounds__(NP*(TL > 0 ? TL : kSweepTL), PPMLR_SWEEP_V2_MI
         tma_load_fields<AXIS, NP, TL, DIPOLE>(A, M, idn, NXT, &s_mbar[buf ^ 1]);
       }
     };
-    if (!PPMLR_SWEEP_V2_RSMEM) prefetch();
+    if (!late_pf<AXIS>()) prefetch();
     mbar_wait(&s_mbar[buf], (unsigned)(i >> 1) & 1u);
     bool stored = false;
     bool moved = false;
