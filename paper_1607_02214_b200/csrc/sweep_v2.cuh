@@ -51,15 +51,15 @@ namespace PPMLR_KNS {
 // other buffer every warp waited for it before P3 (the largest stall of
 // the blast z sweep, profiles/r02).  Blast sweep -0.8%, C5 neutral; a
 // request after P4 instead: -0.1%.
-#ifndef PPMLR_SWEEP_V2_RSMEM_Z
-#define PPMLR_SWEEP_V2_RSMEM_Z 0
+#ifndef PPMLR_SWEEP_V2_RSMEM_AXES
+#define PPMLR_SWEEP_V2_RSMEM_AXES 3  // bit a: axis a keeps right states in shared memory
 #endif
 #ifndef PPMLR_SWEEP_V2_LATE_PF_Z
 #define PPMLR_SWEEP_V2_LATE_PF_Z 0
 #endif
 template <int AXIS>
 __device__ constexpr bool rs_of() {
-  return PPMLR_SWEEP_V2_RSMEM && (AXIS != 2 || PPMLR_SWEEP_V2_RSMEM_Z);
+  return PPMLR_SWEEP_V2_RSMEM && ((PPMLR_SWEEP_V2_RSMEM_AXES >> AXIS) & 1);
 }
 template <int AXIS>
 __device__ constexpr bool late_pf() {
