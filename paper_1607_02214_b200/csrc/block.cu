@@ -530,6 +530,15 @@ void choose_sweep_tiles(ppmlr_gpu_block* b) {
       const int nseg = (n + Lmax - 1) / Lmax;
       L = (n + nseg - 1) / nseg;
       L += L & 1;  // even: the x tile box row (TL doubles) must be a multiple of 16 B
+      // fast build: the second compile-time tile (persistent kernel) when it
+      // costs no more strip positions than the runtime tile, whose threads
+      // round up to whole warps (C3 160/150: fast sweep 0.490 -> 0.478 ms;
+      // strict 0.684 -> 0.705, so strict keeps the runtime tile)
+      const int L2 = kSweepTL2 - 8;
+      const int runtime_pos = nseg * ((kSweepNP * (L + 8) + 31) / 32 * 32) / kSweepNP;
+      if (b->precision == PPMLR_FAST && env_int("PPMLR_SWEEP_RUNTIME_TL", 0) == 0 &&
+          env_int("PPMLR_SWEEP_TL2_ON", 1) && (n + L2 - 1) / L2 * kSweepTL2 <= runtime_pos)
+        L = L2;
     }
     b->sweep_L[a] = L;
     const int T = kSweepNP * (L + 8);

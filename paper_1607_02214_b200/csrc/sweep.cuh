@@ -55,8 +55,12 @@ namespace ppmlr_b200 {
 #ifndef PPMLR_SWEEP_TL
 #define PPMLR_SWEEP_TL 72  // strip positions per tile (L + 8; even)
 #endif
+#ifndef PPMLR_SWEEP_TL2
+#define PPMLR_SWEEP_TL2 64  // second compile-time tile (L = 56) for axes < 256 cells
+#endif
 constexpr int kSweepNP = PPMLR_SWEEP_NP;
 constexpr int kSweepTL = PPMLR_SWEEP_TL;
+constexpr int kSweepTL2 = PPMLR_SWEEP_TL2;
 #ifndef PPMLR_SWEEP_MINB
 #define PPMLR_SWEEP_MINB 3  // resident CTAs per SM the register budget targets
 #endif
