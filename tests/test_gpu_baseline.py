@@ -135,12 +135,15 @@ def test_bench_workload_c5_magnetosphere_fast_vs_strict(gpu):
 
 
 @pytest.mark.parametrize("dims,dipole", [((300, 20, 12), False), ((20, 260, 14), False),
-                                         ((18, 12, 290), False), ((264, 36, 20), True)])
+                                         ((18, 12, 290), False), ((264, 36, 20), True),
+                                         ((66, 64, 290), True)])
 def test_fast_partial_compile_time_tiles_within_tolerance(gpu, dims, dipole):
     """Axes >= 256 cells that are not a multiple of 64 take the compile-time
     tile with a partial last segment (and partial pencil groups on the
     short axes): the persistent fast kernel (sweep_v2.cuh) against the
-    strict one-shot kernel, 8 steps, blast physics / the magnetosphere."""
+    strict one-shot kernel, 8 steps, blast physics / the magnetosphere.
+    (66, 64, 290) with the dipole: the y and z sweeps read B_d from the
+    bricks (block.cu bd_bricks_kernel) with a partial last x group."""
     from paper_1607_02214_b200.api import AxisSpec, HarnessOptions
     out = {}
     for prec in ("strict", "fast"):
