@@ -170,14 +170,26 @@ def _oracle_from_host(oracle, gpu, specs, opts, ic):
                               st["bd"], st["frozen_idx"], st["frozen_states"])
 
 
+def _magnetosphere_bricks():
+    # y, z on the compile-time tile (64) with x = 66: the persistent kernel's
+    # y / z sweeps read B_d from the bricks, the last x group partial
+    from paper_1607_02214_b200 import configs
+    from paper_1607_02214_b200.api import AxisSpec
+    c = configs.magnetosphere_small()
+    c.specs[:] = [AxisSpec(-48.0, -48.0 + 66 * 1.2, -48.0, -48.0 + 66 * 1.2, 1.2, 66, 1.05)] + [
+        AxisSpec(-38.4, 38.4, -38.4, 38.4, 1.2, 64, 1.05)] * 2
+    return c
+
+
 @pytest.mark.parametrize("cfg,steps", [("briowu", 30), ("orszag_tang", 8), ("blast", 6),
-                                       ("magnetosphere_small", 6)])
+                                       ("magnetosphere_small", 6), ("magnetosphere_bricks", 4)])
 def test_harness_bitwise_vs_oracle(gpu, oracle, cfg, steps):
     from paper_1607_02214_b200 import configs
     c = {"briowu": lambda: configs.brio_wu(nx=128),
          "orszag_tang": lambda: configs.orszag_tang(n=64),
          "blast": lambda: configs.blast(n=32, radius=0.2),
-         "magnetosphere_small": lambda: configs.magnetosphere_small()}[cfg]()
+         "magnetosphere_small": lambda: configs.magnetosphere_small(),
+         "magnetosphere_bricks": _magnetosphere_bricks}[cfg]()
     h = _harness(gpu, c.specs, c.options, c.ic)
     ob = _oracle_from_host(oracle, gpu, c.specs, c.options, c.ic)
     o = oracle.opts(boundary=c.options.boundary, cfl=c.options.cfl,
