@@ -214,7 +214,8 @@ int ppmlr_gpu_block_state_view(ppmlr_gpu_block* b, double** field_planes, long l
  * core. */
 int ppmlr_gpu_block_init_ic(ppmlr_gpu_block* b, int kind, const double* params);
 /* The dipole field B_d (3 planes, same layout as the state) or NULLs;
- * returns 1 when the block carries one. */
+ * returns 1 when the block carries one.  Read-only: the y/z sweeps read
+ * brick copies of B_d built at upload / init (change B_d via upload). */
 int ppmlr_gpu_block_dipole_view(ppmlr_gpu_block* b, double** bd_planes);
 /* Error word check (host sync): returns the status of the first failure
  * recorded since the last check, with the reference's message. */

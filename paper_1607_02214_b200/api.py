@@ -227,7 +227,9 @@ class Block:
     def state_view(self, interior=True, dipole=False):
         """The device-resident state as 8 torch tensors (z, y, x) viewing the
         library's memory (no copy; valid until the next step or upload);
-        dipole=True: the 3 B_d planes instead (None without a dipole)."""
+        dipole=True: the 3 B_d planes instead (None without a dipole) --
+        read-only: the y/z sweeps read B_d from brick copies the library
+        builds at upload, so B_d changes go through Block.upload."""
         import torch
         pl = (C.c_void_p * 8)()
         st = (C.c_longlong * 3)()
