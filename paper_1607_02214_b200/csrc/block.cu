@@ -989,8 +989,12 @@ int ppmlr_gpu_block_create(const ppmlr_gpu_block_desc* d, ppmlr_gpu_block** out)
       if ((e = cudaMalloc(&b->bdz[a - 1], sizeof(double) * 3 * b->bdz_cs[a - 1])) !=
           cudaSuccess)
         return fail(cuda_fail(e, "cudaMalloc(bd bricks)"));
+      // consistent with the zeroed B_d planes until the first upload
+      if ((e = cudaMemset(b->bdz[a - 1], 0, sizeof(double) * 3 * b->bdz_cs[a - 1])) !=
+          cudaSuccess)
+        return fail(cuda_fail(e, "cudaMemset(bd bricks)"));
     }
-    b->bd_dirty = true;
+    b->bd_dirty = false;
   }
   if ((e = cudaMalloc(&b->d_err, 64)) != cudaSuccess) return fail(cuda_fail(e, "cudaMalloc"));
   b->d_step = b->d_err + 1;
