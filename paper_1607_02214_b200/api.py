@@ -287,7 +287,8 @@ class Harness:
             self.h = None
 
     def __del__(self):
-        self.close()
+        if getattr(N, "lib", None) is not None:  # not at interpreter teardown
+            self.close()
 
     def __enter__(self):
         return self
