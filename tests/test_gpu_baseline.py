@@ -188,3 +188,30 @@ def test_row_interleaved_layout_reproduces_reference(gpu, monkeypatch, name, pre
     if precision == "strict":
         assert digest(out["rows"]) == rec["final_sha"]
     assert np.array_equal(out["rows"].view(np.int64), out["planar"].view(np.int64))
+
+
+@pytest.mark.parametrize("precision", ["strict", "fast"])
+def test_bd_reupload_rebuilds_the_bricks(gpu, precision):
+    """The y/z sweeps read B_d from brick copies (block.cu bd_bricks_kernel):
+    re-uploading a block with a different B_d must reach them.  A harness
+    that stepped with one dipole and was then re-uploaded with a scaled
+    dipole equals a fresh harness given the scaled dipole, bit for bit."""
+    import sys
+    sys.path.insert(0, os.path.dirname(__file__))
+    from test_gpu_parity import _magnetosphere_bricks
+    c = _magnetosphere_bricks()
+    c.options.precision = precision
+    st = gpu.host_block_state(c.specs, (1, 1, 1), c.options, 0, c.ic)
+    bd2 = np.ascontiguousarray(st["bd"] * 1.5)
+    out = []
+    for warm in (True, False):
+        h = gpu.Harness(c.specs, (1, 1, 1), c.options)
+        blk = h.block(0)
+        if warm:
+            blk.upload(st["fields"], st["bd"], st["frozen_idx"], st["frozen_states"])
+            h.run(2)
+        blk.upload(st["fields"], bd2, st["frozen_idx"], st["frozen_states"])
+        h.run(3)
+        out.append(h.gather_interior())
+        h.close()
+    assert np.array_equal(out[0].view(np.int64), out[1].view(np.int64))
