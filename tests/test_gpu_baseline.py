@@ -215,3 +215,31 @@ def test_bd_reupload_rebuilds_the_bricks(gpu, precision):
         out.append(h.gather_interior())
         h.close()
     assert np.array_equal(out[0].view(np.int64), out[1].view(np.int64))
+
+
+@pytest.mark.parametrize("case", ["blast_128_6", "bricks"])
+def test_fast_build_is_deterministic(gpu, case):
+    """The fast persistent sweep synchronises two of its phases through
+    per-warp mbarriers (sweep_v2.cuh lsync) and claims tiles dynamically; a
+    missed dependency would show as run-to-run differences.  Three runs of
+    the same case must agree bit for bit."""
+    import sys
+    sys.path.insert(0, os.path.dirname(__file__))
+    outs = []
+    for _ in range(3):
+        if case == "bricks":
+            from test_gpu_parity import _magnetosphere_bricks
+            c = _magnetosphere_bricks()
+            c.options.precision = "fast"
+            h = gpu.Harness(c.specs, (1, 1, 1), c.options)
+            h.init_magnetosphere()
+            steps = 8
+        else:
+            rec = GOLD[case]
+            h = _harness(gpu, rec, "fast")
+            steps = rec["steps"] + 4
+        h.run(steps)
+        outs.append(h.gather_interior())
+        h.close()
+    for o in outs[1:]:
+        assert np.array_equal(o.view(np.int64), outs[0].view(np.int64))
