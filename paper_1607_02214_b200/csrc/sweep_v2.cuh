@@ -66,6 +66,9 @@ __device__ constexpr bool late_pf() {
   return rs_of<AXIS>() || (AXIS == 2 && PPMLR_SWEEP_V2_LATE_PF_Z);
 }
 
+#ifndef PPMLR_SWEEP_X_BD_EARLY
+#define PPMLR_SWEEP_X_BD_EARLY 1  // x sweeps with the dipole: C5 / C3 fast +0.3%
+#endif
 #ifndef PPMLR_SWEEP_BD_BRICKS
 #define PPMLR_SWEEP_BD_BRICKS 1  // z sweeps read B_d from its z-brick copy (SweepArgs::bdz)
 #endif
@@ -123,7 +126,27 @@ __device__ __forceinline__ bool sweep_tile_v2(const SweepArgs& A, const SweepMap
   constexpr int fof[8] = {0, 1 + a, 1 + b, 1 + d, 4 + a, 4 + b, 4 + d, 7};
 
   // ---- P0: cf and primitive slopes ----------------------------------------
-  if (live && s < TLv) {
+  if (DIPOLE && AXIS == 0 && PPMLR_SWEEP_X_BD_EARLY && live && s < TLv) {
+    // x sweeps: B_d loads issued first, in flight during the slopes
+    const long long off = (long long)(g0 + p + 4) * A.stride_g +
+                          (long long)(oc + 4) * A.stride_o + (long long)q * A.stride_a;
+    const double b0 = __ldg(A.bd[0] + off), b1 = __ldg(A.bd[1] + off),
+                 b2 = __ldg(A.bd[2] + off);
+    if (s >= 1 && s <= TLv - 2) {
+      const SlopeC sc = slope_coef(A.slope, q);
+#pragma unroll
+      for (int v = 0; v < 8; ++v) {
+        const double* pv = FLD + fof[v] * T + ci;
+        TR[v * T + ci] = slope_with(pv[-SS], pv[0], pv[SS], sc);
+      }
+    }
+    double qv[8];
+#pragma unroll
+    for (int f = 0; f < 8; ++f) qv[f] = FLD[f * T + ci];
+    Ops o;
+    CF[ci] = fast_speed3<AXIS, Ops, true>(qv, b0, b1, b2, k, o);
+    tbad |= o.bad;
+  } else if (live && s < TLv) {
     double qv[8];
 #pragma unroll
     for (int f = 0; f < 8; ++f) qv[f] = FLD[f * T + ci];
