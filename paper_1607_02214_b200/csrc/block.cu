@@ -225,7 +225,7 @@ __global__ void wind_fill_kernel(Planes s, Lay L, const double* bd0, const doubl
   }
 }
 
-// B_d planes -> z-bricks (SweepArgs::bdz): one thread per brick element,
+// B_d planes -> y / z bricks (SweepArgs::bdz): one thread per brick element,
 // the padding pencils of a partial last x group are zero.
 // axis 1: o = z, strip position y; axis 2: o = y, strip position z.
 __global__ void bd_bricks_kernel(double* __restrict__ bdz, const double* __restrict__ bd,
@@ -392,7 +392,7 @@ double* cur_buf(ppmlr_gpu_block* b) { return b->buf[b->cur]; }
 // buffer 0, the 8 of buffer 1 and the 3 B_d components follow each other
 // ([z][y][field][x], field stride P0, y stride NF*P0), so that a z-sweep
 // tile touches 72 2 MB pages instead of 72 per field.  Measured (DESIGN.md
-// §6): the C5 z sweep -2.4%, the blast 512^3 z sweep +18%; planar stays.
+// §4): the C5 z sweep -2.4%, the blast 512^3 z sweep +18%; planar stays.
 void set_state_layout(ppmlr_gpu_block* b) {
   b->P0 = ((b->S[0] + 7) / 8) * 8;
   const char* env = std::getenv("PPMLR_LAYOUT");
