@@ -160,29 +160,29 @@ __global__ void bc_kernel(Planes s, Lay L, BcAxes ax, int layers, int mode) {
   const int na = axis == 0 ? L.n0 : (axis == 1 ? L.n1 : L.n2);
   const int nb = axis == 0 ? L.n1 : (axis == 1 ? L.n2 : L.n0);
   const int nc = axis == 0 ? L.n2 : (axis == 1 ? L.n0 : L.n1);
-  const long long per_side = (long long)layers * nb * nc;
-  const long long total = 2 * per_side;
-  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
-       t += (long long)gridDim.x * blockDim.x) {
-    const int side = (int)(t / per_side);
-    const long long r = t - side * per_side;
+  // 32-bit index arithmetic (a face slab has < 2^31 cells: launch_bc)
+  const int per_side = layers * nb * nc;
+  const int total = 2 * per_side;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+    const int side = t >= per_side;
+    const int r = t - side * per_side;
     // layer fastest for axis 0 (contiguous), transverse fastest otherwise
     int layer, t1, t2;
     if (axis == 0) {
-      layer = 1 + (int)(r % layers);
-      t1 = (int)((r / layers) % nb);
-      t2 = (int)(r / ((long long)layers * nb));
-    } else {
-      // iterate x fastest: for axis 1, x = t2 (d axis); for axis 2, x = t1 (b axis)
-      if (axis == 1) {
-        t2 = (int)(r % nc);
-        t1 = (int)((r / nc) % nb);
-        layer = 1 + (int)(r / ((long long)nc * nb));
-      } else {
-        t1 = (int)(r % nb);
-        t2 = (int)((r / nb) % nc);
-        layer = 1 + (int)(r / ((long long)nb * nc));
-      }
+      const int rl = r / layers;
+      layer = 1 + (r - rl * layers);
+      t2 = rl / nb;
+      t1 = rl - t2 * nb;
+    } else if (axis == 1) {  // iterate x fastest: x = t2 (d axis)
+      const int rn = r / nc;
+      t2 = r - rn * nc;
+      layer = 1 + rn / nb;
+      t1 = rn - (layer - 1) * nb;
+    } else {  // x = t1 (b axis)
+      const int rn = r / nb;
+      t1 = r - rn * nb;
+      layer = 1 + rn / nc;
+      t2 = rn - (layer - 1) * nc;
     }
     if (side == 0 && !phys_lo) continue;
     if (side == 1 && !phys_hi) continue;
@@ -647,6 +647,10 @@ int launch_bc(ppmlr_gpu_block* b, int axis_mask, int layers) {
     work = std::max(work, 2LL * layers * b->n[(a + 1) % 3] * b->n[(a + 2) % 3]);
   }
   if (na == 0) return 0;
+  if (work >= (1LL << 31)) {
+    set_error("apply_boundaries: face slab too large for one launch");
+    return PPMLR_INVALID_SPEC;
+  }
   bc_kernel<<<dim3(grid_for(work), na), 256, 0, b->stream>>>(s, L, ax, layers, b->boundary);
   b->kernel_launches += 1;
   CK(cudaGetLastError());
