@@ -313,17 +313,19 @@ __global__ void pack_kernel(Planes s, Lay L, int face, int layers, double* out) 
   const int na = axis == 0 ? L.n0 : (axis == 1 ? L.n1 : L.n2);
   const int nb = axis == 0 ? L.n1 : (axis == 1 ? L.n2 : L.n0);
   const int nc = axis == 0 ? L.n2 : (axis == 1 ? L.n0 : L.n1);
-  const long long total = (long long)nb * nc * layers;
-  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
-       t += (long long)gridDim.x * blockDim.x) {
-    const int q = (int)(t % layers);
-    const int t1 = (int)((t / layers) % nb);
-    const int t2 = (int)(t / ((long long)layers * nb));
+  // 32-bit index arithmetic: a face slab of >= 2^31 cells would need a
+  // block beyond any GPU's memory
+  const int total = nb * nc * layers;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+    const int tl = t / layers;
+    const int q = t - tl * layers;
+    const int t2 = tl / nb;
+    const int t1 = tl - t2 * nb;
     int cell[3];
     face_cell(axis, t1, t2, face % 2 == 0 ? q : na - layers + q, cell);
     const long long d = L.idx(cell[0], cell[1], cell[2]);
 #pragma unroll
-    for (int f = 0; f < 8; ++f) out[t * 8 + f] = s.f[f][d];
+    for (int f = 0; f < 8; ++f) out[(long long)t * 8 + f] = s.f[f][d];
   }
 }
 
@@ -334,17 +336,19 @@ __global__ void unpack_kernel(Planes s, Lay L, int face, int layers, const doubl
   const int nb = axis == 0 ? L.n1 : (axis == 1 ? L.n2 : L.n0);
   const int nc = axis == 0 ? L.n2 : (axis == 1 ? L.n0 : L.n1);
   const int src_face = face ^ 1;
-  const long long total = (long long)nb * nc * layers;
-  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
-       t += (long long)gridDim.x * blockDim.x) {
-    const int q = (int)(t % layers);
-    const int t1 = (int)((t / layers) % nb);
-    const int t2 = (int)(t / ((long long)layers * nb));
+  // 32-bit index arithmetic: a face slab of >= 2^31 cells would need a
+  // block beyond any GPU's memory
+  const int total = nb * nc * layers;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+    const int tl = t / layers;
+    const int q = t - tl * layers;
+    const int t2 = tl / nb;
+    const int t1 = tl - t2 * nb;
     int cell[3];
     face_cell(axis, t1, t2, src_face % 2 == 0 ? na + q : -layers + q, cell);
     const long long d = L.idx(cell[0], cell[1], cell[2]);
 #pragma unroll
-    for (int f = 0; f < 8; ++f) s.f[f][d] = in[t * 8 + f];
+    for (int f = 0; f < 8; ++f) s.f[f][d] = in[(long long)t * 8 + f];
   }
 }
 
@@ -355,12 +359,14 @@ __global__ void copy_face_kernel(Planes dst, Lay Ld, Planes src, Lay Ls, int fac
   const int nb = axis == 0 ? Ld.n1 : (axis == 1 ? Ld.n2 : Ld.n0);
   const int nc = axis == 0 ? Ld.n2 : (axis == 1 ? Ld.n0 : Ld.n1);
   const int src_face = face ^ 1;
-  const long long total = (long long)nb * nc * layers;
-  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
-       t += (long long)gridDim.x * blockDim.x) {
-    const int q = (int)(t % layers);
-    const int t1 = (int)((t / layers) % nb);
-    const int t2 = (int)(t / ((long long)layers * nb));
+  // 32-bit index arithmetic: a face slab of >= 2^31 cells would need a
+  // block beyond any GPU's memory
+  const int total = nb * nc * layers;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+    const int tl = t / layers;
+    const int q = t - tl * layers;
+    const int t2 = tl / nb;
+    const int t1 = tl - t2 * nb;
     int cs[3], cd[3];
     face_cell(axis, t1, t2, src_face % 2 == 0 ? q : nas - layers + q, cs);
     face_cell(axis, t1, t2, src_face % 2 == 0 ? nad + q : -layers + q, cd);
