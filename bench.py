@@ -428,10 +428,11 @@ def bench_e2e(h, cfg, args, cells):
     h.advance()
     blk.download_interior(out=host_out)
     torch.cuda.synchronize()
-    # wall clock is exposed to host jitter: short passes (< 1 s) are timed
-    # three times and the best is kept
-    best = None
-    for _ in range(3):
+    # wall clock is exposed to host jitter (a 45 ms C3 pass moved by 20 ms
+    # between runs): passes shorter than 1 s are repeated, up to 10 or 2 s
+    # in all, and the best is kept
+    best, spent = None, 0.0
+    for n in range(10):
         t0 = time.perf_counter()
         blk.upload(host_in, host_bd, st["frozen_idx"], st["frozen_states"])
         for _ in range(k):
@@ -439,14 +440,16 @@ def bench_e2e(h, cfg, args, cells):
         blk.download_interior(out=host_out)
         t1 = time.perf_counter()
         best = t1 - t0 if best is None else min(best, t1 - t0)
-        if t1 - t0 >= 1.0:
+        spent += t1 - t0
+        if t1 - t0 >= 1.0 or (n >= 2 and spent >= 2.0):
             break
     h2d = host_in.nbytes + (host_bd.nbytes if host_bd is not None else 0)
     d2h = host_out.nbytes + 8 * k
     return {"value": cells * k / best, "unit": UNIT,
             "h2d_bytes_per_step": h2d / k, "d2h_bytes_per_step": d2h / k,
             "how": f"upload(pinned) + {k} x advance() + download_interior(pinned), wall "
-                   "clock, after one untimed pass; best of 3 passes when a pass is < 1 s"}
+                   "clock, after one untimed pass; passes under 1 s repeated (up to 10, "
+                   "2 s in all) and the best kept"}
 
 
 def bench_reference(args):
